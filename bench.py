@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: zeta + Möbius round trip (one "step" = kernels iii, iv, v and
+the chain difference over one batch) on the BASELINE.json metric
+"zeta/Möbius n·k gathers/s and HBM GB/s vs peak, at 1/2/4/8 B200".
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C5w] [--impl ours|reference]
+
+* Workload (default): C5w = BASELINE.json configs[4] (n=16M random window DAG,
+  W=64, B=32 fp64) in its width-bounded reading (R1); the literal
+  C5 needs a 161 TB dense table.  Setup (one-time) is timed
+  separately and reported under "setup".
+* Multi-GPU: torchrun, one process per GPU; batched functions shard by column
+  (each rank transforms its own B columns: weak scaling, no data-path
+  collective).  Time = max over ranks of CUDA-event time.
+* value: n·k·B gathers per transform x 2 transforms x steps x ranks / time.
+* e2e: same metric through the C-ABI with pinned HOST buffers (H2D + D2H in
+  the timed region).
+* roofline: the dominant kernel's algorithmic bytes / its CUDA-event time
+  recorded by the library on the launching stream inside the timed region.
+* cpu_baseline / --impl reference: the CPU oracle O2 (the paper's sequential
+  Algs. 3-4 in plain C, oracle/chain_oracle.c) on a bounded prefix sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PHASES = ("scan", "gather", "moebius_solve", "chain_diff")
+KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
+                "moebius_solve": "k_moeb_* (v)", "chain_diff": "k_chain_diff"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5w")
+    ap.add_argument("--dtype", default=None, choices=[None, "i64", "f64"])
+    ap.add_argument("--batch", type=int, default=None, help="functions per rank")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--moebius-kernel", default="auto", choices=["auto", "level", "grid", "warp"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="oracle prefix size")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def alg_bytes(n, k, B):
+    """Algorithmic bytes per launch of each phase."""
+    return {
+        "scan": 16 * n * B + 4 * n,                 # f read, F write, slot->user
+        "gather": 4 * n * k + 16 * n * B + 4 * n,   # index stream, F read once, g write
+        "moebius_solve": 4 * n * k + 24 * n * B + 8 * n,   # index, g read, F write + read once
+        "chain_diff": 16 * n * B + 4 * n,
+    }
+
+
+def oracle_sample(wl, B, n_sample, dtype):
+    """Time the CPU oracle O2 (Algs. 3 + 4, single thread) on the down-closed
+    prefix of the workload's first n_sample vertices (generator ids are
+    bottom-up, so the prefix is itself a poset of the same family)."""
+    import numpy as np
+    import workloads as W
+    from oracle.chain import ChainOracle
+    m = wl.src < n_sample
+    src, dst = wl.src[m], wl.dst[m]
+    O = ChainOracle(n_sample, src, dst)
+    if dtype == "i64":
+        f = W.int_values(n_sample, B, -1000, 1000, seed=1)
+    else:
+        f = W.normal_values(n_sample, B, seed=1)
+    t0 = time.perf_counter()
+    g = O.zeta(f)
+    O.moebius(g)
+    dt = time.perf_counter() - t0
+    return {"n": n_sample, "k": O.k, "nnz": O.nnz, "B": B, "seconds": dt,
+            "units": 2 * n_sample * O.k * B}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    import workloads as W
+    wl = W.make_workload(args.config, args.scale, args.dtype, args.batch)
+    n_s = args.cpu_sample or min(wl.n, 400_000)
+    for _ in range(args.warmup):
+        oracle_sample(wl, wl.batch, n_s, wl.dtype)
+    tot_t, tot_u, last = 0.0, 0, None
+    for _ in range(args.steps):
+        r = oracle_sample(wl, wl.batch, n_s, wl.dtype)
+        tot_t += r["seconds"]
+        tot_u += r["units"]
+        last = r
+    value = tot_u / tot_t
+    sample = (f"prefix n={n_s} of {args.config} (k={last['k']}, nnz={last['nnz']}), B={wl.batch} "
+              f"{wl.dtype}, zeta+Möbius Algs. 3-4 single thread, setup excluded")
+    line = {"impl": "reference", "metric": "zeta/Möbius n·k gathers/s", "value": value,
+            "unit": "n·k·B gathers/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": wl.dtype, "data": "synthetic",
+            "config": {"workload": args.config, "n": wl.n, "batch_per_rank": wl.batch},
+            "cpu_baseline": {"value": value, "unit": "n·k·B gathers/s", "cores": 1,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "n·k·B gathers/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    import numpy as np
+    import torch
+    import paper_2211_13706_b200 as pz
+    import workloads as W
+    torch.cuda.set_device(local)
+    wl = W.make_workload(args.config, args.scale, args.dtype, args.batch)
+    B = wl.batch
+    t0 = time.perf_counter()
+    P = pz.Poset(wl.n, wl.src, wl.dst, device=local)
+    setup_s = time.perf_counter() - t0
+    info = P.info()
+    kern = {"auto": 0, "level": 1, "grid": 2, "warp": 3}[args.moebius_kernel]
+    P.set_option("moebius_kernel", kern)
+    f_host = wl.values(seed=1 + rank)
+    x = torch.from_numpy(f_host).cuda()
+    g = torch.empty_like(x)
+    y = torch.empty_like(x)
+    n, k = info["n"], info["k"]
+
+    def step():
+        P.zeta(x, out=g)
+        P.moebius(g, out=y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness spot check of the timed computation (round trip)
+    if wl.dtype == "i64":
+        ok = bool(torch.equal(y, x))
+    else:
+        ok = None   # fp64 Möbius on deep posets is ill-conditioned (R8)
+    P.set_option("profile", 1)
+    P.profile_read()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    prof, launches = P.profile_read()
+    P.set_option("profile", 0)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    units_step = 2 * n * k * B
+    value = world * units_step * args.steps / (ms_max / 1e3)
+
+    # per-kernel roofline (this rank; rank 0 reports)
+    peak, peak_kind = peaks()
+    ab = alg_bytes(n, k, B)
+    kernels = {}
+    for ph in PHASES:
+        tms, calls = prof[ph]
+        if calls == 0:
+            continue
+        per = tms / calls
+        gbs = ab[ph] / (per / 1e3) / 1e9
+        kernels[ph] = {"kernel": KERNEL_NAMES[ph], "ms_per_call": per, "share": tms / ms,
+                       "alg_bytes": ab[ph], "achieved_gbs": gbs, "frac": gbs / peak}
+    dom = max(kernels, key=lambda p: kernels[p]["share"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "achieved": kernels[dom]["achieved_gbs"],
+            "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": kernels[dom]["frac"],
+            "traffic": traffic}
+    if dom == "moebius_solve":
+        roof["note"] = (f"latency-bound triangular solve: {info['ell']} dependent levels, "
+                        f"{1e6 * kernels[dom]['ms_per_call'] / 1e3 / max(info['ell'], 1):.1f} µs per level")
+
+    # e2e: C-ABI with pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        fp = torch.from_numpy(f_host).pin_memory()
+        gp = torch.empty_like(fp).pin_memory()
+        P.zeta(fp, out=gp)
+        P.moebius(gp, out=gp)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.e2e_steps):
+            P.zeta(fp, out=gp)
+            P.moebius(gp, out=gp)
+        a1.record()
+        torch.cuda.synchronize()
+        ems = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
+        ems = float(ems.item())
+        e2e = {"value": world * units_step * args.e2e_steps / (ems / 1e3), "unit": "n·k·B gathers/s",
+               "h2d_bytes_per_step": 2 * n * B * 8, "d2h_bytes_per_step": 2 * n * B * 8,
+               "ms_per_step": ems / args.e2e_steps}
+        del fp, gp
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s = args.cpu_sample or min(wl.n, 1_000_000)
+        r = oracle_sample(wl, B, n_s, wl.dtype)
+        cpu = {"value": r["units"] / r["seconds"], "unit": "n·k·B gathers/s", "cores": 1,
+               "kind": "oracle",
+               "sample": (f"prefix n={n_s} of {args.config} (k={r['k']}, nnz={r['nnz']}), B={B} "
+                          f"{wl.dtype}, one zeta + one Möbius (Algs. 3-4), setup excluded, "
+                          f"{r['seconds']:.2f} s")}
+
+    if rank == 0:
+        line = {
+            "metric": "zeta/Möbius n·k gathers/s", "value": value, "unit": "n·k·B gathers/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+            "config": {"workload": args.config, "desc": wl.desc, "n": n, "k": k,
+                       "batch_per_rank": B, "global_batch": B * world, "ell": info["ell"],
+                       "q": info["q"], "nnz": info["nnz"], "edges": info["m"],
+                       "moebius_kernel": ["auto", "level", "grid", "warp"][info["moebius_kernel"]],
+                       "parallelism": f"column-shard x{world}",
+                       "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
+            "gbs_per_step": (alg_bytes(n, k, B)["scan"] + alg_bytes(n, k, B)["gather"] +
+                             alg_bytes(n, k, B)["moebius_solve"] + alg_bytes(n, k, B)["chain_diff"])
+                            / (ms_max / args.steps / 1e3) / 1e9,
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk, "round_trip_exact": ok,
+            "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
+                      "match": info["t_match"], "chains": info["t_chains"],
+                      "upload": info["t_upload"], "mtable": info["t_mtable"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,223 @@
+/*
+ * poset.h -- C-ABI of the B200-native chain-decomposition zeta / Moebius
+ * transforms (arXiv 2211.13706, "Fast Möbius and zeta transforms on posets";
+ * paper text at /root/reference/PAPER.md, cited as P:Lnnn).
+ *
+ * Library: paper_2211_13706_b200/libposet.so (sm_100a CUDA + host C++).
+ * Every step of the transforms runs in this library's CUDA kernels; there is
+ * no CPU fallback.  A missing GPU makes every compute call return POSET_ECUDA.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions
+ * ---------------------------------------------------------------------------
+ *  Vertices   dense user ids 0..n-1.  Ids are never renumbered at the ABI.
+ *  Edges      (src[e], dst[e]) means dst ⪯ src: dst is a successor of src in
+ *             the DAG.  Duplicates are ignored, isolated vertices
+ *             are singleton chains, the DAG need not be connected (reading
+ *             G11 of DESIGN.md).
+ *  Functions  f, g are row-major [n][batch] arrays (batch contiguous), in
+ *             USER vertex order.  dtype POSET_I64 computes in Z/2^64
+ *             (two's-complement wraparound, reading G14); POSET_F64 uses
+ *             IEEE binary64 adds/subtracts (no multiplies).
+ *  Pointers   f, g may be device pointers (any CUDA allocation on the
+ *             handle's device) or host pointers (pinned or pageable).  Host
+ *             buffers are staged through device buffers owned by the handle
+ *             (H2D copy, kernels, D2H copy, all on `stream`); the host result
+ *             is valid once `stream` has synchronised.  f == g is allowed.
+ *  Streams    `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *             default stream).  Compute calls are asynchronous and
+ *             stream-ordered; setup is synchronous.
+ *  Threads    a handle is not re-entrant: serialise calls per handle.
+ *  Errors     return codes, never exceptions; poset_last_error() gives the
+ *             calling thread's last message.  CUDA failures are sticky in the
+ *             handle (POSET_ECUDA).
+ *
+ * Internal layout: elements are ranked in level order
+ * (Alg. 6 antichains, bottom-up, ties by user id); chains are
+ * laid out contiguously ("slots"), chain j occupying slots off_j..off_j+len_j-1
+ * bottom-up.  The reachability table is chain-major int32 M[k][n]:
+ * M[j][r] = off_j + m(r, j) where m(x,j) = max{p : chain_j[p] ⪯ x}
+ * (= the paper's niv_j(x), as a position), or n when
+ * ↓x ∩ Z_j = ∅ (the paper's ∞, mapped to an all-zero row of F).
+ */
+#ifndef POSET_H
+#define POSET_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct poset_s *poset_t;
+
+typedef enum {
+    POSET_OK = 0,
+    POSET_EINVAL = 1,         /* bad argument: null pointer, id out of range, batch <= 0, range  */
+    POSET_ESELFLOOP = 2,      /* an edge (u, u) (S:L48 SelfLoopError)                           */
+    POSET_ECYCLE = 3,         /* the edges contain a directed cycle (S:L48 CycleError)           */
+    POSET_ENOTCHAIN = 4,      /* injected chain with consecutive incomparable elements  */
+    POSET_ENOTPARTITION = 5,  /* injected chains do not partition 0..n-1                */
+    POSET_ETOOBIG = 6,        /* dense n*k*4-byte table + buffers exceed free device memory      */
+    POSET_ENOMEM = 7,         /* host allocation failed                                          */
+    POSET_ECUDA = 8           /* CUDA error (no device, launch failure, ...) -- sticky           */
+} poset_status;
+
+typedef enum { POSET_I64 = 0, POSET_F64 = 1 } poset_dtype;
+
+/* Moebius U-solve strategies (kernel v). */
+typedef enum {
+    POSET_MOEB_AUTO = 0,      /* cost model picks one of the below                       */
+    POSET_MOEB_LEVEL = 1,     /* one launch per antichain level (Alg. 5)     */
+    POSET_MOEB_GRID = 2,      /* persistent cooperative kernel, grid barrier per level   */
+    POSET_MOEB_WARP = 3       /* one warp per column group sweeps all levels (no grid sync) */
+} poset_moebius_kernel;
+
+typedef struct {
+    int64_t n;            /* elements                                               */
+    int64_t m;            /* distinct edges after de-duplication                    */
+    int64_t k;            /* chains (minimum path cover of E, reading G1)           */
+    int64_t q;            /* longest chain of the decomposition            */
+    int64_t ell;          /* antichain levels = poset length (Thm. 5)       */
+    int64_t nnz;          /* finite niv entries incl. self entries = nnz(N)*/
+    int64_t table_bytes;  /* bytes of the dense chain-major int32 table (4*n*k)     */
+    int64_t max_level_width;
+    double t_ingest;      /* seconds: validate, de-duplicate, CSR                   */
+    double t_levels;      /* seconds: Alg. 6 levels + ranks                         */
+    double t_match;       /* seconds: Alg. 1 maximum matching (augmenting paths)    */
+    double t_chains;      /* seconds: chain walk, slots                             */
+    double t_upload;      /* seconds: host -> device copies                         */
+    double t_mtable;      /* seconds: kernel (ii) + nnz count                       */
+    int32_t device;
+    int32_t moebius_kernel; /* strategy AUTO resolves to (poset_moebius_kernel)     */
+} poset_info;
+
+/*
+ * poset_setup -- one-time precomputation for the poset given by the DAG
+ * (n vertices, m edges src[e] -> dst[e], host int64 arrays).  Runs Alg. 6
+ * levels, Alg. 1 chain decomposition by maximum matching on the
+ * split graph (augmenting paths), and kernel (ii): the table M by
+ * level-sequential max propagation, Thm. 4.  Synchronous.
+ * device: CUDA ordinal.  On success *out owns all device memory of the poset.
+ * Errors: EINVAL, ESELFLOOP, ECYCLE, ETOOBIG, ENOMEM, ECUDA.
+ */
+poset_status poset_setup(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                         int device, poset_t *out);
+
+/*
+ * poset_setup_chains -- as poset_setup, but with an injected chain
+ * decomposition (SPEC decompose_explicit): chain c is
+ * chain_elems[chain_ptr[c] .. chain_ptr[c+1]) listed TOP-DOWN (largest first),
+ * user ids.  Consecutive elements must be comparable (ENOTCHAIN); the chains
+ * must partition 0..n-1 (ENOTPARTITION).  Test hook: reproduces the paper's N.
+ */
+poset_status poset_setup_chains(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                                int64_t k, const int64_t *chain_ptr, const int64_t *chain_elems,
+                                int device, poset_t *out);
+
+/*
+ * poset_zeta -- g = Z f, g(x) = Σ_{y ⪯ x} f(y)  (Eq. inv-formula P:L13;
+ * fast form Eq. zeta-fast P:L401-407 / Alg. 3, factorised as
+ * Z = U V, Eq. zfac): kernel (iii) segmented chain scan F = V f,
+ * then kernel (iv) gather-reduce g(x) = Σ_j F[M[j][x]].
+ * f, g: [n][batch], see Conventions.  Errors: EINVAL, ECUDA.
+ */
+poset_status poset_zeta(poset_t h, const void *f, void *g, int64_t batch, poset_dtype dt,
+                        void *stream);
+
+/*
+ * poset_moebius -- f = Z^{-1} g = M g, f(x) = Σ_{y ⪯ x} μ(y,x) g(y)
+ * (Eq. inv-formula, Cor. 1 P:L143-151; fast form P:L499-502 / Alg. 4
+ * P:L645-674): kernel (v) back-substitution x = U y' in level order
+ * (F(x) = g(x) - Σ_{j≠id(x)} F[M[j][x]]), then the chain difference
+ * f(x) = F(x) - F(next(x)) (V^{-1}).  g, f: [n][batch].
+ * Errors: EINVAL, ECUDA.
+ */
+poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, poset_dtype dt,
+                           void *stream);
+
+/* ---- split phases for row-sharded single-function zeta ----
+ * A rank owning slot range [slot_lo, slot_hi) and rank-row range
+ * [row_lo, row_hi) runs:
+ *   poset_scan_slots(f -> F[slot_lo:slot_hi], carry_in = 0, tail out)
+ *   (all-gather the tails over NCCL, combine them -> carry_in)
+ *   poset_scan_carry(F[slot_lo:slot_hi] += carry_in up to the first chain start)
+ *   (all-gather F over NCCL)
+ *   poset_gather_rows(F -> g rows [row_lo, row_hi) in rank order)
+ * F is a device array [n+1][batch] in slot order; the caller owns it and must
+ * keep row n zero.  tail: device [2][batch] (word 0 of column b = 1 if the
+ * range contains a chain start else 0; word 1 = sum of the values after the
+ * last chain start in the range, or of all values if none).
+ */
+poset_status poset_scan_slots(poset_t h, const void *f, void *F, void *tail, int64_t slot_lo,
+                              int64_t slot_hi, int64_t batch, poset_dtype dt, void *stream);
+poset_status poset_scan_carry(poset_t h, void *F, const void *carry_in, int64_t slot_lo,
+                              int64_t slot_hi, int64_t batch, poset_dtype dt, void *stream);
+poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t row_lo,
+                               int64_t row_hi, int64_t batch, poset_dtype dt, void *stream);
+/* carry_out[b] = value of the segmented prefix of tails_all[0..rank-1]
+ * (device [world][2][batch] as written by poset_scan_slots on each rank), the
+ * carry into rank `rank`'s slot range. */
+poset_status poset_combine_tails(poset_t h, const void *tails_all, int64_t world, int64_t rank,
+                                 void *carry_out, int64_t batch, poset_dtype dt, void *stream);
+/* g_user[user(r)] = g_rank[r] for all ranks r (device arrays [n][batch]). */
+poset_status poset_rank_to_user(poset_t h, const void *g_rank, void *g_user, int64_t batch,
+                                poset_dtype dt, void *stream);
+
+/*
+ * poset_analyze -- HOST-ONLY part of the setup (no GPU needed): ingest,
+ * Alg. 6 levels, Alg. 1 chain decomposition.  Fills out->n, m, k, q, ell,
+ * max_level_width, table_bytes (= 4*n*k, the dense table poset_setup would
+ * allocate) and the host timings; nnz = -1.  chain/pos/level (nullable, host
+ * int64 [n]): per user vertex chain id, bottom-up position, level.  Used to
+ * report the literal configs' k and table size (POSET_ETOOBIG decision)
+ * without a device, and by the CPU test-suite.
+ */
+poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                           poset_info *out, int64_t *chain, int64_t *pos, int64_t *level);
+
+/* poset_query -- sizes, timings and the resolved Moebius strategy. */
+poset_status poset_query(poset_t h, poset_info *out);
+
+/* poset_set_option -- "moebius_kernel" (poset_moebius_kernel value);
+ * "profile" (0/1): record a CUDA event pair on the call's stream around every
+ * kernel phase of subsequent calls (see poset_profile_read). */
+poset_status poset_set_option(poset_t h, const char *key, int64_t value);
+
+/* Profiling phases. */
+enum {
+    POSET_PH_SCAN = 0,      /* kernel (iii)   */
+    POSET_PH_GATHER = 1,    /* kernel (iv)    */
+    POSET_PH_MSOLVE = 2,    /* kernel (v)     */
+    POSET_PH_DIFF = 3,      /* chain difference */
+    POSET_PH_H2D = 4,       /* host staging in  */
+    POSET_PH_D2H = 5,       /* host staging out */
+    POSET_PH_COUNT = 8
+};
+
+/* poset_profile_read -- synchronise the recorded events, return per phase the
+ * summed milliseconds (ms[POSET_PH_COUNT]), the number of timed calls
+ * (calls[POSET_PH_COUNT]) and the number of kernel launches the library made
+ * since the last read (*launches), then reset.  Any pointer may be NULL. */
+poset_status poset_profile_read(poset_t h, double *ms, int64_t *calls, int64_t *launches);
+
+/*
+ * Test / inspection hooks (copy device state to caller-owned HOST arrays):
+ *  poset_export_chains: per user vertex x: chain[x] (0..k-1), pos[x] (bottom-up
+ *    position, 0 = lowest), level[x] (0 = leaves), rank[x].
+ *  poset_export_mtable: out[x*k + j] = m(x, j) (position, -1 = ∞), user order;
+ *    n*k int32 host array.
+ */
+poset_status poset_export_chains(poset_t h, int64_t *chain, int64_t *pos, int64_t *level,
+                                 int64_t *rank);
+poset_status poset_export_mtable(poset_t h, int32_t *out);
+
+void poset_destroy(poset_t h);
+const char *poset_strerror(poset_status s);
+const char *poset_last_error(void);
+int poset_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POSET_H */

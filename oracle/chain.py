@@ -42,6 +42,8 @@ def _load():
             fn.restype = ctypes.c_int
         lib.oracle_zeta_sampled.argtypes = [P, P, i64, ctypes.c_int, i64, P, P, P]
         lib.oracle_zeta_sampled.restype = ctypes.c_int
+        lib.oracle_zeta_sampled_edges.argtypes = [i64, i64, P, P, P, i64, ctypes.c_int, i64, P, P, P]
+        lib.oracle_zeta_sampled_edges.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -135,3 +137,24 @@ class ChainOracle:
         if rc:
             raise MemoryError("oracle_zeta_sampled")
         return g, ab
+
+
+def zeta_sampled_edges(n, src, dst, f, xs):
+    """Brute-force g(x) = Σ_{y ⪯ x} f(y) for user vertices ``xs`` straight
+    from the edge list (DFS of ↓x; no chains, no niv).  For fp64 also
+    returns Σ_{y ⪯ x}|f(y)| (the tolerance scale)."""
+    lib = _load()
+    src = np.ascontiguousarray(src, dtype=np.int64)
+    dst = np.ascontiguousarray(dst, dtype=np.int64)
+    f = np.ascontiguousarray(f).reshape(n, -1)
+    xs = np.ascontiguousarray(xs, dtype=np.int64)
+    B = f.shape[1]
+    dt = 0 if f.dtype == np.int64 else 1
+    g = np.empty((xs.shape[0], B), dtype=f.dtype)
+    ab = np.empty((xs.shape[0], B), dtype=np.float64) if dt == 1 else None
+    rc = lib.oracle_zeta_sampled_edges(n, src.shape[0], _ptr(src), _ptr(dst), _ptr(f), B, dt,
+                                       xs.shape[0], _ptr(xs), _ptr(g),
+                                       _ptr(ab) if ab is not None else None)
+    if rc:
+        raise MemoryError("oracle_zeta_sampled_edges")
+    return g, ab

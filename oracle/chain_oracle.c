@@ -526,3 +526,55 @@ int oracle_zeta_sampled(const oracle_poset *P, const void *fin, int64_t B, int d
     free(stk); free(seen);
     return 0;
 }
+
+/* ---------------- brute-force sampled zeta straight from the edge list ----
+ * For full-size sampled parity (no matching, no niv): builds the children
+ * CSR and sums f over ↓x by DFS for each listed x (definition).
+ * dtype 0 int64 (Z/2^64), 1 fp64 (+ Σ|f| into abs_out if non-null). */
+int oracle_zeta_sampled_edges(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                              const void *fin, int64_t B, int dtype, int64_t ns,
+                              const int64_t *xs, void *gout, double *abs_out) {
+    int64_t *cp = calloc((size_t)n + 1, sizeof(int64_t));
+    int64_t *ci = malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+    int64_t *stk = malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    int64_t *seen = malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    if (!cp || !ci || !stk || !seen) return -4;
+    for (int64_t e = 0; e < m; e++) cp[src[e] + 1]++;
+    for (int64_t v = 0; v < n; v++) cp[v + 1] += cp[v];
+    int64_t *fill = malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    memcpy(fill, cp, sizeof(int64_t) * (size_t)n);
+    for (int64_t e = 0; e < m; e++) ci[fill[src[e]]++] = dst[e];
+    free(fill);
+    for (int64_t v = 0; v < n; v++) seen[v] = -1;
+    for (int64_t s = 0; s < ns; s++) {
+        int64_t sp = 0;
+        stk[sp++] = xs[s];
+        seen[xs[s]] = s;
+        if (dtype == 0) {
+            const uint64_t *f = fin; uint64_t *g = (uint64_t *)gout + (size_t)s * B;
+            for (int64_t b = 0; b < B; b++) g[b] = 0;
+            while (sp) {
+                int64_t v = stk[--sp];
+                for (int64_t b = 0; b < B; b++) g[b] += f[(size_t)v * B + b];
+                for (int64_t t = cp[v]; t < cp[v + 1]; t++)
+                    if (seen[ci[t]] != s) { seen[ci[t]] = s; stk[sp++] = ci[t]; }
+            }
+        } else {
+            const double *f = fin; double *g = (double *)gout + (size_t)s * B;
+            double *ga = abs_out ? abs_out + (size_t)s * B : NULL;
+            for (int64_t b = 0; b < B; b++) { g[b] = 0; if (ga) ga[b] = 0; }
+            while (sp) {
+                int64_t v = stk[--sp];
+                for (int64_t b = 0; b < B; b++) {
+                    double x = f[(size_t)v * B + b];
+                    g[b] += x;
+                    if (ga) ga[b] += x < 0 ? -x : x;
+                }
+                for (int64_t t = cp[v]; t < cp[v + 1]; t++)
+                    if (seen[ci[t]] != s) { seen[ci[t]] = s; stk[sp++] = ci[t]; }
+            }
+        }
+    }
+    free(cp); free(ci); free(stk); free(seen);
+    return 0;
+}

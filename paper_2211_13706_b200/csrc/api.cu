@@ -1,0 +1,570 @@
+// C-ABI of libposet.so -- see include/poset.h for the contract of every entry
+// point.  Host setup (setup.cpp) + device residency + kernel launches
+// (kernels.cu).  No compute step runs on the host: every transform step is a
+// CUDA kernel; without a GPU every compute call returns POSET_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+using namespace poset;
+
+static thread_local std::string g_last_error;
+
+static poset_status fail(poset_status s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+
+struct poset_s {
+    int device = 0;
+    int num_sms = 148;
+    HostPoset H;
+    poset_info info{};
+    int moeb_opt = MOEB_AUTO;
+    cudaError_t sticky = cudaSuccess;
+    // device residency
+    int32_t *d_rank_user = nullptr, *d_slot = nullptr, *d_chain = nullptr, *d_lvl = nullptr;
+    int32_t *d_child = nullptr, *d_slot_user = nullptr, *d_M = nullptr;
+    int64_t *d_child_ptr = nullptr;
+    unsigned *d_bar = nullptr;
+    unsigned long long *d_count = nullptr;
+    // scratch, grown on demand
+    void *d_F = nullptr;
+    size_t F_bytes = 0;
+    void *d_scan = nullptr;
+    size_t scan_bytes = 0;
+    void *d_part = nullptr;
+    size_t part_bytes = 0;
+    void *d_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes[2] = {0, 0};
+    // profiling: event pairs recorded on the caller's stream per kernel phase
+    bool prof_on = false;
+    struct Rec { int ph; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    DevPoset dev() const {
+        DevPoset P;
+        P.n = H.n;
+        P.k = H.k;
+        P.ell = H.ell;
+        P.rank_user = d_rank_user;
+        P.slot = d_slot;
+        P.chain = d_chain;
+        P.lvl_ptr = d_lvl;
+        P.child_ptr = d_child_ptr;
+        P.child = d_child;
+        P.slot_user = d_slot_user;
+        P.M = d_M;
+        return P;
+    }
+};
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess) {                                                              \
+            if (h) h->sticky = _e;                                                            \
+            return fail(POSET_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+        }                                                                                     \
+    } while (0)
+
+static void free_all(poset_s *h) {
+    if (!h) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->device);
+    for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : h->pool) cudaEventDestroy(e);
+    void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
+                    h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
+                    h->d_stage[0], h->d_stage[1]};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    cudaSetDevice(prev);
+}
+
+template <typename T>
+static cudaError_t upload(T **dst, const std::vector<T> &v) {
+    size_t bytes = std::max<size_t>(v.size(), 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)dst, bytes);
+    if (e != cudaSuccess) return e;
+    if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+static poset_status finish_setup(poset_s *h) {
+    HostPoset &H = h->H;
+    double t0 = now_seconds();
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+    // size guard: dense table + resident arrays + a B=1 F buffer
+    size_t table = (size_t)H.n * (size_t)H.k * 4;
+    size_t resident = table + (size_t)H.n * 4 * 6 + (size_t)H.m * 4 + (size_t)H.n * 8 + 4096;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    h->info.table_bytes = (int64_t)table;
+    h->info.k = H.k;
+    if (resident + (size_t)(H.n + 1) * 8 * 4 > free_b) {
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "poset_setup: dense table needs %.2f GB (n=%d, k=%d) but %.2f GB are free",
+                 table / 1e9, H.n, H.k, free_b / 1e9);
+        return fail(POSET_ETOOBIG, buf);
+    }
+    CK(upload(&h->d_rank_user, H.rank_user));
+    CK(upload(&h->d_slot, H.slot));
+    CK(upload(&h->d_chain, H.chain));
+    CK(upload(&h->d_lvl, H.lvl_ptr));
+    CK(upload(&h->d_child_ptr, H.child_ptr));
+    CK(upload(&h->d_child, H.child));
+    CK(upload(&h->d_slot_user, H.slot_user));
+    CK(cudaMalloc((void **)&h->d_bar, 64));
+    CK(cudaMalloc((void **)&h->d_count, 64));
+    CK(cudaMalloc((void **)&h->d_M, std::max<size_t>(table, 4)));
+    CK(cudaDeviceSynchronize());
+    double t1 = now_seconds();
+    DevPoset P = h->dev();
+    CK(launch_mtable(P, h->d_M, 0));
+    CK(launch_count_nnz(h->d_M, (int64_t)H.n * H.k, H.n, h->d_count, 0));
+    unsigned long long nnz = 0;
+    CK(cudaMemcpy(&nnz, h->d_count, sizeof nnz, cudaMemcpyDeviceToHost));
+    CK(cudaDeviceSynchronize());
+    double t2 = now_seconds();
+    poset_info &I = h->info;
+    I.n = H.n;
+    I.m = H.m;
+    I.k = H.k;
+    I.q = H.q;
+    I.ell = H.ell;
+    I.nnz = (int64_t)nnz;
+    I.max_level_width = H.max_level_width;
+    I.t_ingest = H.t_ingest;
+    I.t_levels = H.t_levels;
+    I.t_match = H.t_match;
+    I.t_chains = H.t_chains;
+    I.t_upload = t1 - t0;
+    I.t_mtable = t2 - t1;
+    I.device = h->device;
+    I.moebius_kernel = moebius_pick(P, 1, H.max_level_width, h->num_sms);
+    // drop host arrays only the device needs
+    std::vector<int32_t>().swap(H.child);
+    std::vector<int64_t>().swap(H.child_ptr);
+    return POSET_OK;
+}
+
+static poset_status setup_common(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                                 int64_t k, const int64_t *cp, const int64_t *ce, bool inject,
+                                 int device, poset_t *out) {
+    if (!out) return fail(POSET_EINVAL, "poset_setup: out is null");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t ce_ = cudaGetDeviceCount(&ndev);
+    if (ce_ != cudaSuccess || ndev == 0)
+        return fail(POSET_ECUDA, std::string("poset_setup: no CUDA device: ") + cudaGetErrorString(ce_));
+    if (device < 0 || device >= ndev) return fail(POSET_EINVAL, "poset_setup: bad device ordinal");
+    poset_s *h = new (std::nothrow) poset_s();
+    if (!h) return fail(POSET_ENOMEM, "poset_setup: out of host memory");
+    h->device = device;
+    std::string err;
+    poset_status st;
+    try {
+        st = host_ingest(n, m, src, dst, h->H, err);
+        if (st == POSET_OK)
+            st = inject ? host_chains_injected(h->H, k, cp, ce, err) : host_chains_matching(h->H, err);
+    } catch (const std::bad_alloc &) {
+        st = POSET_ENOMEM;
+        err = "poset_setup: out of host memory";
+    }
+    if (st != POSET_OK) {
+        delete h;
+        return fail(st, err);
+    }
+    st = finish_setup(h);
+    if (st != POSET_OK) {
+        free_all(h);
+        delete h;
+        return st;
+    }
+    *out = h;
+    return POSET_OK;
+}
+
+extern "C" {
+
+poset_status poset_setup(int64_t n, int64_t m, const int64_t *src, const int64_t *dst, int device,
+                         poset_t *out) {
+    return setup_common(n, m, src, dst, 0, nullptr, nullptr, false, device, out);
+}
+
+poset_status poset_setup_chains(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                                int64_t k, const int64_t *chain_ptr, const int64_t *chain_elems,
+                                int device, poset_t *out) {
+    return setup_common(n, m, src, dst, k, chain_ptr, chain_elems, true, device, out);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- helpers ----
+static poset_status grow(poset_s *h, void **p, size_t *cap, size_t need) {
+    if (need <= *cap) return POSET_OK;
+    if (*p) {
+        CK(cudaFree(*p));
+        *p = nullptr;
+        *cap = 0;
+    }
+    CK(cudaMalloc(p, need));
+    *cap = need;
+    return POSET_OK;
+}
+
+static poset_status check_call(poset_s *h, const void *a, const void *b, int64_t batch, int dt,
+                               const char *fn) {
+    if (!h) return fail(POSET_EINVAL, std::string(fn) + ": null handle");
+    if (h->sticky != cudaSuccess)
+        return fail(POSET_ECUDA, std::string(fn) + ": sticky CUDA error: " + cudaGetErrorString(h->sticky));
+    if (batch <= 0) return fail(POSET_EINVAL, std::string(fn) + ": batch must be > 0");
+    if (dt != POSET_I64 && dt != POSET_F64) return fail(POSET_EINVAL, std::string(fn) + ": bad dtype");
+    if (h->H.n > 0 && (!a || !b)) return fail(POSET_EINVAL, std::string(fn) + ": null data pointer");
+    if ((int64_t)h->H.n * batch > ((int64_t)1 << 40))
+        return fail(POSET_EINVAL, std::string(fn) + ": n*batch too large");
+    return POSET_OK;
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static poset_status ensure_F(poset_s *h, int64_t batch, cudaStream_t s) {
+    size_t need = (size_t)(h->H.n + 1) * batch * 8;
+    poset_status st = grow(h, &h->d_F, &h->F_bytes, need);
+    if (st) return st;
+    // row n is the all-zero target of ∞ entries (reading G12)
+    CK(cudaMemsetAsync((char *)h->d_F + (size_t)h->H.n * batch * 8, 0, (size_t)batch * 8, s));
+    return POSET_OK;
+}
+
+// CUDA-event timer around one kernel phase (only when profiling is on)
+struct PhaseTimer {
+    poset_s *h;
+    int ph;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    static cudaEvent_t get(poset_s *h) {
+        cudaEvent_t e = nullptr;
+        if (!h->pool.empty()) { e = h->pool.back(); h->pool.pop_back(); }
+        else cudaEventCreate(&e);
+        return e;
+    }
+    PhaseTimer(poset_s *h_, int ph_, cudaStream_t s_) : h(h_), ph(ph_), s(s_) {
+        if (h->prof_on) { a = get(h); cudaEventRecord(a, s); }
+    }
+    void end() {
+        if (!a) return;
+        cudaEvent_t b = get(h);
+        cudaEventRecord(b, s);
+        h->recs.push_back({ph, a, b});
+        a = nullptr;
+    }
+    ~PhaseTimer() { end(); }
+};
+
+typedef poset_status (*device_fn)(poset_s *, const void *, void *, int64_t, int, cudaStream_t);
+
+static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int dt, cudaStream_t s) {
+    poset_status st = ensure_F(h, B, s);
+    if (st) return st;
+    st = grow(h, &h->d_scan, &h->scan_bytes, scan_scratch_bytes(h->H.n, B));
+    if (st) return st;
+    size_t pb = gather_partial_bytes(h->dev(), h->H.n, B, h->num_sms);
+    if (pb) {
+        st = grow(h, &h->d_part, &h->part_bytes, pb);
+        if (st) return st;
+    }
+    DevPoset P = h->dev();
+    {
+        PhaseTimer t(h, POSET_PH_SCAN, s);
+        CK(launch_scan(P, dt, f, h->d_F, 0, h->H.n, B, h->d_scan, nullptr, s));
+    }
+    {
+        PhaseTimer t(h, POSET_PH_GATHER, s);
+        CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, h->num_sms, s));
+    }
+    return POSET_OK;
+}
+
+static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, int dt, cudaStream_t s) {
+    poset_status st = ensure_F(h, B, s);
+    if (st) return st;
+    DevPoset P = h->dev();
+    int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
+                                         : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+    h->info.moebius_kernel = which;
+    {
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_solve(P, h->H.lvl_ptr.data(), dt, g, h->d_F, B, which, h->d_bar,
+                                h->num_sms, s));
+    }
+    {
+        PhaseTimer t(h, POSET_PH_DIFF, s);
+        CK(launch_chain_diff(P, dt, h->d_F, f, B, s));
+    }
+    return POSET_OK;
+}
+
+// Host buffers (and device buffers not 32-byte aligned, which the 256-bit
+// vector loads/stores need) are staged through handle-owned device buffers:
+// copy in, kernels, copy out -- all on `s`.
+static poset_status run_staged(poset_s *h, device_fn fn, const void *in, void *out, int64_t B,
+                               int dt, cudaStream_t s) {
+    bool din = is_device_ptr(in) && ((uintptr_t)in % 32) == 0;
+    bool dout = is_device_ptr(out) && ((uintptr_t)out % 32) == 0;
+    size_t bytes = (size_t)h->H.n * B * 8;
+    const void *src = in;
+    void *dst = out;
+    if (!din) {
+        poset_status st = grow(h, &h->d_stage[0], &h->stage_bytes[0], bytes);
+        if (st) return st;
+        PhaseTimer t(h, POSET_PH_H2D, s);
+        CK(cudaMemcpyAsync(h->d_stage[0], in, bytes, cudaMemcpyDefault, s));
+        src = h->d_stage[0];
+    }
+    if (!dout) {
+        poset_status st = grow(h, &h->d_stage[1], &h->stage_bytes[1], bytes);
+        if (st) return st;
+        dst = h->d_stage[1];
+    }
+    poset_status st = fn(h, src, dst, B, dt, s);
+    if (st) return st;
+    if (!dout) {
+        PhaseTimer t(h, POSET_PH_D2H, s);
+        CK(cudaMemcpyAsync(out, dst, bytes, cudaMemcpyDefault, s));
+    }
+    return POSET_OK;
+}
+
+extern "C" {
+
+poset_status poset_zeta(poset_t h, const void *f, void *g, int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, f, g, batch, dt, "poset_zeta");
+    if (st || h->H.n == 0) return st;
+    CK(cudaSetDevice(h->device));
+    return run_staged(h, zeta_dev, f, g, batch, dt, (cudaStream_t)stream);
+}
+
+poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, poset_dtype dt,
+                           void *stream) {
+    poset_status st = check_call(h, g, f, batch, dt, "poset_moebius");
+    if (st || h->H.n == 0) return st;
+    CK(cudaSetDevice(h->device));
+    return run_staged(h, moebius_dev, g, f, batch, dt, (cudaStream_t)stream);
+}
+
+poset_status poset_scan_slots(poset_t h, const void *f, void *F, void *tail, int64_t lo, int64_t hi,
+                              int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, f, F, batch, dt, "poset_scan_slots");
+    if (st) return st;
+    if (lo < 0 || hi > h->H.n || lo > hi || !tail) return fail(POSET_EINVAL, "poset_scan_slots: bad range");
+    CK(cudaSetDevice(h->device));
+    st = grow(h, &h->d_scan, &h->scan_bytes, scan_scratch_bytes(hi - lo, batch));
+    if (st) return st;
+    CK(launch_scan(h->dev(), dt, f, F, lo, hi, batch, h->d_scan, tail, (cudaStream_t)stream));
+    return POSET_OK;
+}
+
+poset_status poset_scan_carry(poset_t h, void *F, const void *carry, int64_t lo, int64_t hi,
+                              int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, F, carry, batch, dt, "poset_scan_carry");
+    if (st) return st;
+    if (lo < 0 || hi > h->H.n || lo > hi) return fail(POSET_EINVAL, "poset_scan_carry: bad range");
+    // the carry reaches the rows before the first chain start at or after lo
+    const std::vector<int32_t> &off = h->H.chain_off;
+    auto itr = std::lower_bound(off.begin(), off.end() - 1, (int32_t)lo);
+    int64_t end = itr == off.end() - 1 ? hi : std::min<int64_t>(hi, *itr);
+    CK(cudaSetDevice(h->device));
+    CK(launch_scan_carry(h->dev(), dt, F, carry, lo, end, batch, (cudaStream_t)stream));
+    return POSET_OK;
+}
+
+poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t lo, int64_t hi,
+                               int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, F, g_rank, batch, dt, "poset_gather_rows");
+    if (st) return st;
+    if (lo < 0 || hi > h->H.n || lo > hi) return fail(POSET_EINVAL, "poset_gather_rows: bad range");
+    CK(cudaSetDevice(h->device));
+    size_t pb = gather_partial_bytes(h->dev(), hi - lo, batch, h->num_sms);
+    if (pb) {
+        st = grow(h, &h->d_part, &h->part_bytes, pb);
+        if (st) return st;
+    }
+    CK(launch_gather(h->dev(), dt, F, g_rank, lo, hi, batch, 1, pb ? h->d_part : nullptr, h->num_sms,
+                     (cudaStream_t)stream));
+    return POSET_OK;
+}
+
+poset_status poset_combine_tails(poset_t h, const void *tails_all, int64_t world, int64_t rank,
+                                 void *carry_out, int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, tails_all, carry_out, batch, dt, "poset_combine_tails");
+    if (st) return st;
+    if (world <= 0 || rank < 0 || rank >= world) return fail(POSET_EINVAL, "poset_combine_tails: bad rank");
+    CK(cudaSetDevice(h->device));
+    CK(launch_combine_tails(dt, tails_all, world, rank, carry_out, batch, (cudaStream_t)stream));
+    return POSET_OK;
+}
+
+poset_status poset_rank_to_user(poset_t h, const void *g_rank, void *g_user, int64_t batch,
+                                poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, g_rank, g_user, batch, dt, "poset_rank_to_user");
+    if (st) return st;
+    CK(cudaSetDevice(h->device));
+    CK(launch_rank_to_user(h->dev(), dt, g_rank, g_user, batch, (cudaStream_t)stream));
+    return POSET_OK;
+}
+
+poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                           poset_info *out, int64_t *chain, int64_t *pos, int64_t *level) {
+    if (!out) return fail(POSET_EINVAL, "poset_analyze: out is null");
+    HostPoset H;
+    std::string err;
+    poset_status st;
+    try {
+        st = host_ingest(n, m, src, dst, H, err);
+        if (st == POSET_OK) st = host_chains_matching(H, err);
+    } catch (const std::bad_alloc &) {
+        st = POSET_ENOMEM;
+        err = "poset_analyze: out of host memory";
+    }
+    if (st != POSET_OK) return fail(st, err);
+    poset_info I{};
+    I.n = H.n;
+    I.m = H.m;
+    I.k = H.k;
+    I.q = H.q;
+    I.ell = H.ell;
+    I.nnz = -1;
+    I.table_bytes = (int64_t)H.n * H.k * 4;
+    I.max_level_width = H.max_level_width;
+    I.t_ingest = H.t_ingest;
+    I.t_levels = H.t_levels;
+    I.t_match = H.t_match;
+    I.t_chains = H.t_chains;
+    I.device = -1;
+    *out = I;
+    for (int32_t r = 0; r < H.n; r++) {
+        int32_t u = H.rank_user[r];
+        if (chain) chain[u] = H.chain[r];
+        if (pos) pos[u] = H.pos[r];
+        if (level) level[u] = H.level[r];
+    }
+    return POSET_OK;
+}
+
+poset_status poset_query(poset_t h, poset_info *out) {
+    if (!h || !out) return fail(POSET_EINVAL, "poset_query: null argument");
+    *out = h->info;
+    return POSET_OK;
+}
+
+poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
+    if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
+    if (!strcmp(key, "moebius_kernel")) {
+        if (value < MOEB_AUTO || value > MOEB_WARP) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        h->moeb_opt = (int)value;
+        return POSET_OK;
+    }
+    if (!strcmp(key, "profile")) {
+        h->prof_on = value != 0;
+        return POSET_OK;
+    }
+    return fail(POSET_EINVAL, std::string("poset_set_option: unknown key ") + key);
+}
+
+poset_status poset_profile_read(poset_t h, double *ms, int64_t *calls, int64_t *launches) {
+    if (!h) return fail(POSET_EINVAL, "poset_profile_read: null handle");
+    double acc[POSET_PH_COUNT] = {0};
+    int64_t cnt[POSET_PH_COUNT] = {0};
+    CK(cudaSetDevice(h->device));
+    for (auto &r : h->recs) {
+        CK(cudaEventSynchronize(r.b));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, r.a, r.b));
+        acc[r.ph] += t;
+        cnt[r.ph]++;
+        h->pool.push_back(r.a);
+        h->pool.push_back(r.b);
+    }
+    h->recs.clear();
+    for (int i = 0; i < POSET_PH_COUNT; i++) {
+        if (ms) ms[i] = acc[i];
+        if (calls) calls[i] = cnt[i];
+    }
+    int64_t l = launches_take();
+    if (launches) *launches = l;
+    return POSET_OK;
+}
+
+poset_status poset_export_chains(poset_t h, int64_t *chain, int64_t *pos, int64_t *level, int64_t *rank) {
+    if (!h || !chain || !pos || !level || !rank) return fail(POSET_EINVAL, "poset_export_chains: null argument");
+    const HostPoset &H = h->H;
+    for (int32_t r = 0; r < H.n; r++) {
+        int32_t u = H.rank_user[r];
+        chain[u] = H.chain[r];
+        pos[u] = H.pos[r];
+        level[u] = H.level[r];
+        rank[u] = r;
+    }
+    return POSET_OK;
+}
+
+poset_status poset_export_mtable(poset_t h, int32_t *out) {
+    if (!h || !out) return fail(POSET_EINVAL, "poset_export_mtable: null argument");
+    const HostPoset &H = h->H;
+    std::vector<int32_t> M((size_t)H.n * H.k);
+    CK(cudaSetDevice(h->device));
+    if (!M.empty()) CK(cudaMemcpy(M.data(), h->d_M, M.size() * 4, cudaMemcpyDeviceToHost));
+    for (int32_t j = 0; j < H.k; j++)
+        for (int32_t r = 0; r < H.n; r++) {
+            int32_t v = M[(size_t)j * H.n + r];
+            out[(size_t)H.rank_user[r] * H.k + j] = v == H.n ? -1 : v - H.chain_off[j];
+        }
+    return POSET_OK;
+}
+
+void poset_destroy(poset_t h) {
+    if (!h) return;
+    free_all(h);
+    delete h;
+}
+
+const char *poset_strerror(poset_status s) {
+    switch (s) {
+        case POSET_OK: return "ok";
+        case POSET_EINVAL: return "invalid argument";
+        case POSET_ESELFLOOP: return "self loop";
+        case POSET_ECYCLE: return "cycle";
+        case POSET_ENOTCHAIN: return "not a chain";
+        case POSET_ENOTPARTITION: return "not a partition";
+        case POSET_ETOOBIG: return "dense table too big for device memory";
+        case POSET_ENOMEM: return "out of host memory";
+        case POSET_ECUDA: return "CUDA error";
+    }
+    return "unknown";
+}
+
+const char *poset_last_error(void) { return g_last_error.c_str(); }
+
+int poset_abi_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL).
+
+Two ways the hot path shards:
+
+* **Batched functions -> column sharding** (``column_shard``): every rank
+  holds the whole poset (replicated index table) and transforms its own
+  B_local columns.  No collective on the data path; weak scaling.
+
+* **Single-function zeta -> row sharding** (``row_sharded_zeta``): rank p
+  owns the slot range S_p and the rank-row range R_p (equal contiguous
+  splits).  It scans S_p (kernel iii, carry-in 0), all-gathers the per-range
+  scan tails (G x 2 x B words), combines them into its carry
+  (``poset_combine_tails``) and adds it to the rows before its first chain
+  start, all-gathers F over NCCL (in place), gathers g for R_p (kernel iv)
+  and all-gathers the rank-ordered g, which ``poset_rank_to_user`` scatters
+  into user order.
+
+Single-function Möbius is not sharded: its U-solve dependency chain
+(depth D_U) does not split across GPUs (north star).
+
+Every arithmetic step runs in libposet.so; this module only sizes ranges and
+calls collectives.  ``emulate_row_sharded_zeta`` runs the same sequence of
+library calls for G emulated ranks on one GPU (the collectives become
+buffer copies), so the split-phase path is testable with one device.
+"""
+from __future__ import annotations
+
+import math
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Equal contiguous split of [0, n): (lo, hi, chunk)."""
+    chunk = max(1, math.ceil(n / world)) if n else 1
+    lo = min(n, rank * chunk)
+    hi = min(n, lo + chunk)
+    return lo, hi, chunk
+
+
+def column_shard(batch: int, world: int, rank: int):
+    """Columns [lo, hi) of a batch of functions owned by ``rank``."""
+    per = math.ceil(batch / world)
+    lo = min(batch, rank * per)
+    return lo, min(batch, lo + per)
+
+
+def _all_gather(out, inp, group=None):
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:   # gloo: list form into contiguous row-chunk views of `out`
+        dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp.contiguous(), group=group)
+
+
+def row_sharded_zeta(P, f, group=None, out=None):
+    """Single-function (or small-batch) zeta sharded by rows over the
+    process group.  ``P``: the rank's Poset (same poset on every rank);
+    ``f``: [n][B] on this rank's device (replicated input).  Returns g
+    [n][B] (user order) on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = P.n
+    f2 = f.reshape(n, -1)
+    B = f2.shape[1]
+    lo, hi, chunk = shard_range(n, world, rank)
+    dev = f.device
+    # F for all slots, padded to world*chunk rows + the zero row n
+    F = torch.zeros((world * chunk + 1, B), dtype=f.dtype, device=dev)
+    tail = torch.zeros((2, B), dtype=f.dtype, device=dev)
+    P.scan_slots(f2, F, tail, lo, hi)
+    tails = torch.empty((world, 2, B), dtype=f.dtype, device=dev)
+    _all_gather(tails.view(world * 2, B), tail, group)
+    carry = torch.zeros((B,), dtype=f.dtype, device=dev)
+    P.combine_tails(tails, world, rank, carry)
+    P.scan_carry(F, carry, lo, hi)
+    _all_gather(F[: world * chunk], F[rank * chunk:(rank + 1) * chunk].clone(), group)
+    F[n].zero_()
+    g_part = torch.zeros((chunk, B), dtype=f.dtype, device=dev)
+    if hi > lo:
+        P.gather_rows(F, g_part, lo, hi)
+    g_rank = torch.empty((world * chunk, B), dtype=f.dtype, device=dev)
+    _all_gather(g_rank, g_part, group)
+    if out is None:
+        out = torch.empty_like(f2)
+    P.rank_to_user(g_rank[:n].contiguous(), out)
+    return out.reshape(f.shape)
+
+
+def emulate_row_sharded_zeta(P, f, world: int):
+    """The call sequence of ``row_sharded_zeta`` for ``world`` emulated ranks
+    on one GPU; each collective becomes a copy.  For tests only -- no kernel
+    waits on another."""
+    import torch
+    n = P.n
+    f2 = f.reshape(n, -1)
+    B = f2.shape[1]
+    chunk = shard_range(n, world, 0)[2]
+    F = torch.zeros((world * chunk + 1, B), dtype=f.dtype, device=f.device)
+    tails = torch.zeros((world, 2, B), dtype=f.dtype, device=f.device)
+    for p in range(world):
+        lo, hi, _ = shard_range(n, world, p)
+        P.scan_slots(f2, F, tails[p], lo, hi)
+    for p in range(world):
+        lo, hi, _ = shard_range(n, world, p)
+        carry = torch.zeros((B,), dtype=f.dtype, device=f.device)
+        P.combine_tails(tails, world, p, carry)
+        P.scan_carry(F, carry, lo, hi)
+    F[n].zero_()
+    g_rank = torch.zeros((world * chunk, B), dtype=f.dtype, device=f.device)
+    for p in range(world):
+        lo, hi, _ = shard_range(n, world, p)
+        if hi > lo:
+            part = torch.zeros((chunk, B), dtype=f.dtype, device=f.device)
+            P.gather_rows(F, part, lo, hi)
+            g_rank[p * chunk:(p + 1) * chunk] = part
+    out = torch.empty_like(f2)
+    P.rank_to_user(g_rank[:n].contiguous(), out)
+    return out.reshape(f.shape)

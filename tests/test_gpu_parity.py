@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north star): int64 bit-exact (Z/2^64); fp64 within
+|Δ| <= 1e-9 * Σ_{y⪯x}|f(y)| (scale computed by the oracle).  Möbius fp64 is
+only compared where μ is bounded (Boolean lattice, shallow posets; reading R8
+of DESIGN.md); deep posets use int64 round trips.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_fp64_close, load_facts, load_matrix
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():   # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2211_13706_b200 as pz  # noqa: E402
+from oracle import brute  # noqa: E402
+from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
+
+KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP]
+facts = load_facts()
+PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def gpu_zeta(P, f):
+    return host(P.zeta(dev(f)))
+
+
+def gpu_moebius(P, g, kernel=None):
+    if kernel is not None:
+        P.set_option("moebius_kernel", kernel)
+    out = host(P.moebius(dev(g)))
+    if kernel is not None:
+        P.set_option("moebius_kernel", pz.MOEB_AUTO)
+    return out
+
+
+# ------------------------------------------------------------ paper example
+
+def test_example_paper_N_and_transforms(paper_example):
+    n, src, dst = paper_example
+    P = pz.Poset(n, src, dst, chains=PAPER_CHAINS)
+    info = P.info()
+    assert info["k"] == 4 and info["nnz"] == int(facts["nnz_N"]) and info["ell"] == 5
+    # N (paper labels, -1 = ∞) -> bottom-up positions
+    N = load_matrix("N.txt")
+    pos = {}
+    for c in PAPER_CHAINS:
+        for p, v in enumerate(reversed(c)):
+            pos[v] = p
+    want = np.where(N > 0, np.vectorize(lambda v: pos.get(v - 1, -1))(N), -1)
+    assert (P.export_mtable() == want).all()
+    Z, M = load_matrix("Z.txt"), load_matrix("M.txt")
+    f = W.int_values(12, 5, -100, 100, seed=3)
+    assert (gpu_zeta(P, f) == Z @ f).all()
+    for kern in KERNELS:
+        assert (gpu_moebius(P, f, kern) == M @ f).all()
+    ff = W.normal_values(12, 4, seed=4)
+    assert_fp64_close(gpu_zeta(P, ff), Z @ ff, Z @ np.abs(ff))
+
+
+def test_example_own_matching(paper_example):
+    n, src, dst = paper_example
+    P = pz.Poset(n, src, dst)
+    assert P.info()["k"] == 4
+    Z, M = load_matrix("Z.txt"), load_matrix("M.txt")
+    f = W.int_values(12, 3, -100, 100, seed=5)
+    assert (gpu_zeta(P, f) == Z @ f).all()
+    assert (gpu_moebius(P, f) == M @ f).all()
+
+
+# ------------------------------------------------------ m-table via Thm. 3
+
+@pytest.mark.parametrize("name,n,make", [
+    ("C1", 1000, lambda: W.window_dag(1000, 3, 50, 0)),
+    ("C5w", 1500, lambda: W.window_dag(1500, 2, 64, 1, forced=True)),
+    ("C4", 8 * 64, lambda: W.layered_dag(8, 64, 3, 2)),
+    ("bool9", 512, lambda: W.boolean_lattice(9)),
+])
+def test_mtable_is_downset_count(name, n, make):
+    """Thm. 3: m(x,j) + 1 = |↓x ∩ Z_j| for the library's own
+    chains; brute-force down-sets from the oracle."""
+    src, dst = make()
+    P = pz.Poset(n, src, dst)
+    chain, pos, level, rank = P.export_chains()
+    mt = P.export_mtable()
+    down = brute.downsets(n, src, dst)
+    k = P.k
+    for x in range(n):
+        members = brute._bits(down[x], n)
+        cnt = np.bincount(chain[members], minlength=k)
+        assert (mt[x] + 1 == cnt).all(), x
+    assert P.info()["nnz"] == int((mt >= 0).sum())
+
+
+# ---------------------------------------------- O2 parity, many instances
+
+def instances():
+    yield "C1", 1000, *W.window_dag(1000, 3, 50, 0)
+    yield "C3lit_20k", 20000, *W.window_dag(20000, 2, 1000, 0)
+    yield "C3w_30k", 30000, *W.window_dag(30000, 2, 1000, 0, forced=True)
+    yield "C4lit_64L", 64 * 256, *W.layered_dag(64, 256, 3, 0)
+    yield "C4w_128L", 128 * 256, *W.layered_dag(128, 256, 3, 0, forced=True)
+    yield "C5lit_20k", 20000, *W.window_dag(20000, 2, 64, 0)
+    yield "C5w_50k", 50000, *W.window_dag(50000, 2, 64, 0, forced=True)
+    yield "bool12", 4096, *W.boolean_lattice(12)
+    yield "ER4_5k", 5000, *W.erdos_renyi(5000, 4, 1)
+    yield "ER6_3k", 3000, *W.erdos_renyi(3000, 6, 2)
+
+
+@pytest.fixture(scope="module")
+def built():
+    cache = {}
+
+    def get(name, n, src, dst):
+        if name not in cache:
+            cache[name] = (pz.Poset(n, src, dst), ChainOracle(n, src, dst))
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("inst", list(instances()), ids=lambda t: t[0])
+@pytest.mark.parametrize("B", [1, 3, 32])
+def test_int64_zeta_moebius_vs_O2(inst, B, built):
+    name, n, src, dst = inst
+    P, O = built(name, n, src, dst)
+    f = W.int_values(n, B, -1000, 1000, seed=B)
+    g = gpu_zeta(P, f)
+    assert (g == O.zeta(f)).all()
+    for kern in KERNELS:
+        if kern == pz.MOEB_LEVEL and P.ell > 3000:
+            continue
+        assert (gpu_moebius(P, g, kern) == f).all(), kern
+    h = W.int_values(n, B, -10**17, 10**17, seed=B + 100)     # arbitrary g, wraps
+    assert (gpu_moebius(P, h) == O.moebius(h)).all()
+
+
+@pytest.mark.parametrize("inst", list(instances()), ids=lambda t: t[0])
+@pytest.mark.parametrize("B", [1, 4])
+def test_fp64_zeta_vs_O2(inst, B, built):
+    name, n, src, dst = inst
+    P, O = built(name, n, src, dst)
+    f = W.normal_values(n, B, seed=7 + B)
+    assert_fp64_close(gpu_zeta(P, f), O.zeta(f), O.zeta(np.abs(f)))
+
+
+@pytest.mark.parametrize("name,n,make", [
+    ("C1", 1000, lambda: W.window_dag(1000, 3, 50, 0)),
+    ("C5w_2k", 2000, lambda: W.window_dag(2000, 2, 64, 0, forced=True)),
+    ("C3w_20k", 20000, lambda: W.window_dag(20000, 2, 1000, 0, forced=True)),
+    ("C4w_24L", 24 * 256, lambda: W.layered_dag(24, 256, 3, 0, forced=True)),
+])
+def test_fp64_moebius_shallow_vs_O2(name, n, make):
+    """fp64 Möbius only where |μ| stays small (reading R8)."""
+    src, dst = make()
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    f = W.normal_values(n, 2, seed=3)
+    g = O.zeta(f)
+    want = O.moebius(g)
+    for kern in KERNELS:
+        assert_fp64_close(gpu_moebius(P, g, kern), want, O.zeta(np.abs(want)))
+
+
+# --------------------------------------------------- C2: Boolean lattice 2^16
+
+def test_C2_boolean_lattice_vs_yates():
+    bits = 16
+    n = 1 << bits
+    src, dst = W.boolean_lattice(bits)
+    P = pz.Poset(n, src, dst)
+    info = P.info()
+    assert info["k"] == 12870 and info["ell"] == 17
+    f = W.normal_values(n, 1, seed=1)
+    g = gpu_zeta(P, f)
+    assert_fp64_close(g, brute.yates_zeta(bits, f), brute.yates_zeta(bits, np.abs(f)))
+    gy = brute.yates_zeta(bits, f)
+    for kern in KERNELS:
+        assert_fp64_close(gpu_moebius(P, gy, kern), brute.yates_moebius(bits, gy),
+                          brute.yates_zeta(bits, np.abs(f)))
+    fi = W.int_values(n, 2, -1000, 1000, seed=2)
+    gi = gpu_zeta(P, fi)
+    assert (gi == brute.yates_zeta(bits, fi)).all()
+    assert (gpu_moebius(P, gi) == fi).all()
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_edge_cases_tiny():
+    for n, (src, dst) in [(1, W.antichain_dag(1)), (7, W.antichain_dag(7)), (40, W.chain_dag(40)),
+                          (2, (np.array([1, 1]), np.array([0, 0])))]:
+        P = pz.Poset(n, src, dst)
+        f = W.int_values(n, 3, -9, 9, seed=n)
+        O = ChainOracle(n, src, dst)
+        assert (gpu_zeta(P, f) == O.zeta(f)).all()
+        assert (gpu_moebius(P, f) == O.moebius(f)).all()
+
+
+def test_ragged_batches_and_1d():
+    n = 3000
+    src, dst = W.window_dag(n, 2, 64, 4, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    for B in (2, 5, 6, 12, 40, 64, 96):
+        f = W.int_values(n, B, -1000, 1000, seed=B)
+        assert (gpu_zeta(P, f) == O.zeta(f)).all(), B
+        assert (gpu_moebius(P, O.zeta(f)) == f).all(), B
+    f1 = W.int_values(n, 1, -5, 5, seed=1)[:, 0]
+    assert (host(P.zeta(dev(f1))) == O.zeta(f1)).all()
+
+
+def test_host_buffers_and_inplace():
+    n = 5000
+    src, dst = W.window_dag(n, 2, 64, 5, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    f = W.int_values(n, 4, -1000, 1000, seed=1)
+    g = P.zeta(f)                      # numpy in/out: staged by the library
+    torch.cuda.synchronize()
+    assert (g == O.zeta(f)).all()
+    pinned = torch.from_numpy(f).pin_memory()
+    out = torch.empty_like(pinned).pin_memory()
+    P.zeta(pinned, out=out)
+    torch.cuda.synchronize()
+    assert (out.numpy() == O.zeta(f)).all()
+    x = dev(f)
+    P.zeta(x, out=x)                   # in place
+    P.moebius(x, out=x)
+    assert (host(x) == f).all()
+
+
+def test_errors_through_abi():
+    with pytest.raises(pz.PosetError) as e:
+        pz.Poset(2, np.array([0, 1]), np.array([1, 0]))
+    assert e.value.code == "ECYCLE"
+    with pytest.raises(pz.PosetError) as e:
+        pz.Poset(2, np.array([1]), np.array([1]))
+    assert e.value.code == "ESELFLOOP"
+    src, dst = W.paper_example_edges()
+    with pytest.raises(pz.PosetError) as e:
+        pz.Poset(12, src, dst, chains=[[2, 3]] + [[v] for v in range(12) if v not in (2, 3)])
+    assert e.value.code == "ENOTCHAIN"
+    with pytest.raises(pz.PosetError) as e:
+        pz.Poset(12, src, dst, chains=[[v] for v in range(11)])
+    assert e.value.code == "ENOTPARTITION"
+    P = pz.Poset(12, src, dst)
+    with pytest.raises(ValueError):
+        P.zeta(dev(np.zeros((11, 1), np.int64)))
+    with pytest.raises(TypeError):
+        P.zeta(dev(np.zeros((12, 1), np.float32)))
+
+
+def test_literal_C3_is_etoobig():
+    n = 1_000_000
+    src, dst = W.window_dag(n, 2, 1000, 0)
+    with pytest.raises(pz.PosetError) as e:
+        pz.Poset(n, src, dst)
+    assert e.value.code == "ETOOBIG"
+
+
+# ------------------------------------------------------ split-phase (dist)
+
+@pytest.mark.parametrize("G", [1, 3, 4])
+def test_split_phase_row_sharded_zeta(G):
+    """Row-sharded single-function zeta (north star): G emulated ranks, each
+    scans its slot range, the tails are combined into carries, the F ranges
+    are concatenated (the all-gather) and each rank gathers its rows."""
+    from paper_2211_13706_b200 import dist
+    n = 40000
+    src, dst = W.window_dag(n, 2, 1000, 0, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    for dtype in ("i64", "f64"):
+        f = W.int_values(n, 2, -1000, 1000, 1) if dtype == "i64" else W.normal_values(n, 2, 1)
+        g = dist.emulate_row_sharded_zeta(P, dev(f), G)
+        got = host(g)
+        if dtype == "i64":
+            assert (got == O.zeta(f)).all()
+        else:
+            assert_fp64_close(got, O.zeta(f), O.zeta(np.abs(f)))
+
+
+# ------------------------------------------------------------ full sizes
+
+def _full_check(name, dtype, B, kernels=(None,)):
+    wl = W.make_workload(name, dtype=dtype, batch=B)
+    P = pz.Poset(wl.n, wl.src, wl.dst)
+    f = wl.values(seed=1)
+    x = dev(f)
+    g = P.zeta(x)
+    rng = np.random.default_rng(0)
+    xs = np.unique(np.concatenate([np.array([0, wl.n - 1]), rng.integers(0, wl.n, 24)]))
+    # bias a few samples low so their down-sets are small enough to DFS quickly
+    want, scale = zeta_sampled_edges(wl.n, wl.src, wl.dst, f, xs)
+    got = host(g)[xs]
+    if dtype == "i64":
+        assert (got == want).all()
+        for kern in kernels:
+            if kern is not None:
+                P.set_option("moebius_kernel", kern)
+            back = host(P.moebius(g))
+            assert (back == f).all(), kern
+    else:
+        assert_fp64_close(got, want, scale)
+    return P
+
+
+@pytest.mark.parametrize("name,dtype,B", [("C3w", "f64", 1), ("C3w", "i64", 1), ("C4w", "i64", 64),
+                                          ("C5w", "i64", 32), ("C5w", "f64", 32)])
+def test_full_size_sampled_and_round_trip(name, dtype, B):
+    _full_check(name, dtype, B)
