@@ -6,7 +6,7 @@ the chain difference over one batch) on the BASELINE.json metric
     python bench.py [--gpus N --steps K --warmup W] [--config C5w] [--impl ours|reference]
 
 * Workload (default): C5w = BASELINE.json configs[4] (n=16M random window DAG,
-  W=64, B=32 fp64) in its width-bounded reading (R1); the literal
+  W=64, B=32 fp64) in its width-bounded reading (reading W1); the literal
   C5 needs a 161 TB dense table.  Setup (one-time) is timed
   separately and reported under "setup".
 * Multi-GPU: torchrun, one process per GPU; batched functions shard by column
@@ -34,9 +34,11 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PHASES = ("scan", "gather", "moebius_solve", "chain_diff")
+PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
-                "moebius_solve": "k_moeb_* (v)", "chain_diff": "k_chain_diff"}
+                "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
+                "chain_diff": "k_chain_diff"}
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring"]
 
 
 def parse():
@@ -49,7 +51,7 @@ def parse():
     ap.add_argument("--dtype", default=None, choices=[None, "i64", "f64"])
     ap.add_argument("--batch", type=int, default=None, help="functions per rank")
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--moebius-kernel", default="auto", choices=["auto", "level", "grid", "warp"])
+    ap.add_argument("--moebius-kernel", default="auto", choices=["auto", "level", "grid", "warp", "ring"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -125,14 +127,20 @@ def dist_init():
     return world, rank, local
 
 
-def alg_bytes(n, k, B):
+def alg_bytes(n, k, B, info=None):
     """Algorithmic bytes per launch of each phase."""
-    return {
+    d = {
         "scan": 16 * n * B + 4 * n,                 # f read, F write, slot->user
         "gather": 4 * n * k + 16 * n * B + 4 * n,   # index stream, F read once, g write
+        "perm": 16 * n * B + 4 * n,                 # g read, gP write, rank->user
         "moebius_solve": 4 * n * k + 24 * n * B + 8 * n,   # index, g read, F write + read once
         "chain_diff": 16 * n * B + 4 * n,
     }
+    if info is not None and info.get("moebius_kernel") == 4:
+        # RING: distance table once (shared by the B CTAs through L2), gP read,
+        # f written, rank->user rows; F never leaves shared memory
+        d["moebius_solve"] = info["dist_bytes"] + 16 * n * B + 4 * n
+    return d
 
 
 def oracle_sample(wl, B, n_sample, dtype):
@@ -204,7 +212,7 @@ def main():
     P = pz.Poset(wl.n, wl.src, wl.dst, device=local)
     setup_s = time.perf_counter() - t0
     info = P.info()
-    kern = {"auto": 0, "level": 1, "grid": 2, "warp": 3}[args.moebius_kernel]
+    kern = MOEB_NAMES.index(args.moebius_kernel)
     P.set_option("moebius_kernel", kern)
     f_host = wl.values(seed=1 + rank)
     x = torch.from_numpy(f_host).cuda()
@@ -223,7 +231,7 @@ def main():
     if wl.dtype == "i64":
         ok = bool(torch.equal(y, x))
     else:
-        ok = None   # fp64 Möbius on deep posets is ill-conditioned (R8)
+        ok = None   # fp64 Möbius on deep posets is ill-conditioned (reading G8)
     P.set_option("profile", 1)
     P.profile_read()
     if world > 1:
@@ -252,7 +260,8 @@ def main():
 
     # per-kernel roofline (this rank; rank 0 reports)
     peak, peak_kind = peaks()
-    ab = alg_bytes(n, k, B)
+    info = P.info()
+    ab = alg_bytes(n, k, B, info)
     kernels = {}
     for ph in PHASES:
         tms, calls = prof[ph]
@@ -322,17 +331,17 @@ def main():
             "config": {"workload": args.config, "desc": wl.desc, "n": n, "k": k,
                        "batch_per_rank": B, "global_batch": B * world, "ell": info["ell"],
                        "q": info["q"], "nnz": info["nnz"], "edges": info["m"],
-                       "moebius_kernel": ["auto", "level", "grid", "warp"][info["moebius_kernel"]],
+                       "moebius_kernel": MOEB_NAMES[info["moebius_kernel"]],
+                       "reach": info["reach"],
                        "parallelism": f"column-shard x{world}",
                        "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
-            "gbs_per_step": (alg_bytes(n, k, B)["scan"] + alg_bytes(n, k, B)["gather"] +
-                             alg_bytes(n, k, B)["moebius_solve"] + alg_bytes(n, k, B)["chain_diff"])
-                            / (ms_max / args.steps / 1e3) / 1e9,
+            "gbs_per_step": sum(ab[p] for p in kernels) / (ms_max / args.steps / 1e3) / 1e9,
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "round_trip_exact": ok,
             "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
                       "match": info["t_match"], "chains": info["t_chains"],
-                      "upload": info["t_upload"], "mtable": info["t_mtable"]},
+                      "upload": info["t_upload"], "mtable": info["t_mtable"],
+                      "dist_table": info["t_dist"]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -70,7 +70,9 @@ typedef enum {
     POSET_MOEB_AUTO = 0,      /* cost model picks one of the below                       */
     POSET_MOEB_LEVEL = 1,     /* one launch per antichain level (Alg. 5)     */
     POSET_MOEB_GRID = 2,      /* persistent cooperative kernel, grid barrier per level   */
-    POSET_MOEB_WARP = 3       /* one warp per column group sweeps all levels (no grid sync) */
+    POSET_MOEB_WARP = 3,      /* one warp per column group sweeps all levels (no grid sync) */
+    POSET_MOEB_RING = 4       /* bounded-reach posets: one CTA per column, F in a shared-memory
+                                 ring, U-solve and chain difference fused   */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -90,6 +92,10 @@ typedef struct {
     double t_mtable;      /* seconds: kernel (ii) + nnz count                       */
     int32_t device;
     int32_t moebius_kernel; /* strategy AUTO resolves to (poset_moebius_kernel)     */
+    int64_t reach;        /* max rank distance from x to a dependency of its U-solve
+                             row or to next(x) (level order); RING needs < 65535     */
+    int64_t dist_bytes;   /* bytes of the RING distance table (0 = RING unavailable)*/
+    double t_dist;        /* seconds: reach + distance table build                  */
 } poset_info;
 
 /*
@@ -192,6 +198,7 @@ enum {
     POSET_PH_DIFF = 3,      /* chain difference */
     POSET_PH_H2D = 4,       /* host staging in  */
     POSET_PH_D2H = 5,       /* host staging out */
+    POSET_PH_PERM = 6,      /* RING: g permuted to rank-major columns */
     POSET_PH_COUNT = 8
 };
 

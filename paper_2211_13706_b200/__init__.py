@@ -23,7 +23,7 @@ import os
 import numpy as np
 
 __all__ = ["Poset", "PosetError", "analyze", "lib", "MOEB_AUTO", "MOEB_LEVEL", "MOEB_GRID", "MOEB_WARP",
-           "LIB_PATH"]
+           "MOEB_RING", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposet.so")
 
@@ -35,7 +35,7 @@ try:
 except OSError as e:   # pragma: no cover
     raise ImportError(f"cannot load {LIB_PATH}: {e} (there is no CPU fallback)") from e
 
-MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP = 0, 1, 2, 3
+MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING = 0, 1, 2, 3, 4
 _I64, _F64 = 0, 1
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -47,7 +47,8 @@ class PosetInfo(ctypes.Structure):
                 ("t_ingest", ctypes.c_double), ("t_levels", ctypes.c_double),
                 ("t_match", ctypes.c_double), ("t_chains", ctypes.c_double),
                 ("t_upload", ctypes.c_double), ("t_mtable", ctypes.c_double),
-                ("device", ctypes.c_int32), ("moebius_kernel", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("moebius_kernel", ctypes.c_int32),
+                ("reach", _i64), ("dist_bytes", _i64), ("t_dist", ctypes.c_double)]
 
 
 def _sig(name, args, res=ctypes.c_int):
@@ -196,7 +197,7 @@ class Poset:
     def set_option(self, key: str, value: int):
         _check(lib.poset_set_option(self._h, key.encode(), int(value)))
 
-    PHASES = ("scan", "gather", "moebius_solve", "chain_diff", "h2d", "d2h")
+    PHASES = ("scan", "gather", "moebius_solve", "chain_diff", "h2d", "d2h", "perm")
 
     def profile_read(self):
         """{phase: (ms summed, calls)} since the last read + kernel launches."""

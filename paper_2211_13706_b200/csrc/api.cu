@@ -36,6 +36,9 @@ struct poset_s {
     int64_t *d_child_ptr = nullptr;
     unsigned *d_bar = nullptr;
     unsigned long long *d_count = nullptr;
+    RingPlan ring;                    // RING Möbius schedule (moebius_ring.cu)
+    void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
+    size_t gP_bytes = 0;
     // scratch, grown on demand
     void *d_F = nullptr;
     size_t F_bytes = 0;
@@ -85,7 +88,7 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1]};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.ru_pad, h->d_gP};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -138,6 +141,40 @@ static poset_status finish_setup(poset_s *h) {
     CK(cudaMemcpy(&nnz, h->d_count, sizeof nnz, cudaMemcpyDeviceToHost));
     CK(cudaDeviceSynchronize());
     double t2 = now_seconds();
+    // RING schedule data: reach of the dependencies, then the rank-major
+    // distance table D if the plan fits shared memory and device memory.
+    {
+        int32_t *d_slot_rank = nullptr;
+        CK(upload(&d_slot_rank, H.slot_rank));
+        unsigned reach = 0;
+        cudaError_t e = launch_reach_max(P, d_slot_rank, (unsigned *)h->d_count, 0);
+        if (e == cudaSuccess) e = cudaMemcpy(&reach, h->d_count, sizeof reach, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { cudaFree(d_slot_rank); CK(e); }
+        ring_plan(H.n, H.k, H.ell, H.max_level_width, reach, h->ring);
+        if (h->ring.ok) {
+            size_t dbytes = (size_t)h->ring.npad * h->ring.kp * 2;
+            size_t fb = 0, tb = 0;
+            cudaMemGetInfo(&fb, &tb);
+            if (dbytes + (size_t)h->ring.npad * 4 + ((size_t)1 << 30) > fb ||
+                cudaMalloc((void **)&h->ring.D, dbytes) != cudaSuccess ||
+                cudaMalloc((void **)&h->ring.ru_pad, (size_t)h->ring.npad * 4) != cudaSuccess) {
+                cudaGetLastError();
+                if (h->ring.D) cudaFree(h->ring.D);
+                h->ring.D = nullptr;
+                h->ring.ok = false;
+            }
+        }
+        if (h->ring.ok) {
+            e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, h->ring.npad, h->ring.D, 0);
+            if (e == cudaSuccess) e = cudaMemset(h->ring.ru_pad, 0, (size_t)h->ring.npad * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(h->ring.ru_pad, h->d_rank_user, (size_t)H.n * 4, cudaMemcpyDeviceToDevice);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { cudaFree(d_slot_rank); CK(e); }
+        }
+        CK(cudaFree(d_slot_rank));
+    }
+    double t3 = now_seconds();
     poset_info &I = h->info;
     I.n = H.n;
     I.m = H.m;
@@ -153,7 +190,10 @@ static poset_status finish_setup(poset_s *h) {
     I.t_upload = t1 - t0;
     I.t_mtable = t2 - t1;
     I.device = h->device;
-    I.moebius_kernel = moebius_pick(P, 1, H.max_level_width, h->num_sms);
+    I.reach = h->ring.reach;
+    I.dist_bytes = h->ring.ok ? (int64_t)h->ring.npad * h->ring.kp * 2 : 0;
+    I.t_dist = t3 - t2;
+    I.moebius_kernel = h->ring.ok ? MOEB_RING : moebius_pick(P, 1, H.max_level_width, h->num_sms);
     // drop host arrays only the device needs
     std::vector<int32_t>().swap(H.child);
     std::vector<int64_t>().swap(H.child_ptr);
@@ -310,8 +350,23 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
     if (st) return st;
     DevPoset P = h->dev();
     int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
-                                         : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+                : h->ring.ok ? MOEB_RING
+                             : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
     h->info.moebius_kernel = which;
+    if (which == MOEB_RING) {
+        if (!h->ring.ok)
+            return fail(POSET_EINVAL, "poset_moebius: the RING schedule does not fit this poset "
+                                      "(reach or rows too large); use AUTO");
+        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->ring.npad * 8);
+        if (st) return st;
+        {
+            PhaseTimer t(h, POSET_PH_PERM, s);
+            CK(launch_to_rank_major(P, dt, g, B, h->ring.npad, h->d_gP, s));
+        }
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_ring(P, h->ring, dt, h->d_gP, f, B, s));
+        return POSET_OK;
+    }
     {
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
         CK(launch_moebius_solve(P, h->H.lvl_ptr.data(), dt, g, h->d_F, B, which, h->d_bar,
@@ -480,7 +535,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_WARP) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RING) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }

@@ -111,6 +111,18 @@ __device__ __forceinline__ void store_row(T *p, const T (&o)[CB]) {
 
 __device__ __forceinline__ int32_t ld_stream_i32(const int32_t *p) { return __ldcs(p); }
 
+// 8-byte read-only load issued only if a != b; the result register is left
+// undefined otherwise.  Opaque to the compiler on purpose: it keeps the
+// predicated loads of a run independent of each other (the C++ form gets
+// rewritten into a chain "dst = previous value; @p ld dst").
+__device__ __forceinline__ u64 ld_nc_if_ne(const void *p, int32_t a, int32_t b) {
+    u64 v;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, %3;\n\t@q ld.global.nc.b64 %0, [%1];\n\t}"
+        : "=l"(v)
+        : "l"(p), "r"(a), "r"(b));
+    return v;
+}
+
 // ---------------------------------------------------- (ii) m-table build --
 // One warp per chain j.  For every level L (bottom-up) and every rank r of L:
 //   M[j][r] = slot(r)                               if chain(r) == j
@@ -394,49 +406,56 @@ cudaError_t launch_combine_tails(int dtype, const void *tails, int64_t world, in
 }
 
 // ---------------------------------------------- (iv) zeta gather-reduce ---
-// Thread = one rank r (32 consecutive ranks per warp -> the chain-major index
-// row M[j][r..r+31] is one coalesced 128-B load), CB consecutive columns.
-// F rows gathered by a warp are near-identical for chain-local posets, so
-// the F loads are L1 broadcasts.  Block id: column group fastest (CTAs of the
-// same tile share the index stream through L2), then j-slice, then tile.
+// Lane = one rank r (a warp owns 32 consecutive ranks, so the chain-major
+// index row M[j][r..r+31] is one coalesced 128-B load); CB <= 8 consecutive
+// columns per thread.  The WG warps of a CTA that own the same 32 ranks take
+// WG different column groups and share each index row through L1
+// (ld.global.nc).  Index loads run U chains ahead of the F loads (register
+// double buffer), which keeps ~U x 128 B of the HBM index stream in flight
+// per warp.  F rows gathered by a warp are near-identical for chain-local
+// posets (1.6-2.4 distinct sectors per warp-gather), so the F
+// loads are L1 broadcasts.  Block id: column-group block fastest, then
+// j-slice, then rank tile.
 template <typename T, int CB, int VEC, int U>
 __global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, int32_t n, int32_t k,
                                                 const T *__restrict__ F, T *__restrict__ out,
                                                 const int32_t *__restrict__ rank_user,
-                                                int64_t row_lo, int64_t row_hi, int32_t B, int G,
-                                                int S, int mode) {
+                                                int64_t row_lo, int64_t row_hi, int32_t B, int GB,
+                                                int WG, int S, int mode) {
     const int64_t bid = blockIdx.x;
-    const int cg = (int)(bid % G);
-    const int64_t rest = bid / G;
+    const int cgb = (int)(bid % GB);
+    const int64_t rest = bid / GB;
     const int slice = (int)(rest % S);
     const int64_t tile = rest / S;
-    const int64_t r = row_lo + tile * 256 + threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wc = warp % WG, wr = warp / WG;
+    const int ranks_per_cta = 32 * (8 / WG);
+    const int64_t r = row_lo + tile * ranks_per_cta + wr * 32 + lane;
     if (r >= row_hi) return;
     const int j0 = (int)((int64_t)slice * k / S), j1 = (int)((int64_t)(slice + 1) * k / S);
-    const int c0 = cg * CB;
+    const int c0 = (cgb * WG + wc) * CB;
     T acc[CB];
 #pragma unroll
     for (int c = 0; c < CB; c++) acc[c] = T(0);
     const int32_t *Mr = M + r;
-    int j = j0;
-    for (; j + U <= j1; j += U) {
-        int32_t idx[U];
+    const T *Fc = F + c0;
+    int32_t idx[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) idx[u] = ld_stream_i32(Mr + (size_t)(j + u) * n);
+    for (int u = 0; u < U; u++) idx[u] = (j0 + u < j1) ? __ldg(Mr + (size_t)(j0 + u) * n) : n;
+    for (int j = j0; j < j1; j += U) {
+        int32_t nidx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            nidx[u] = (j + U + u < j1) ? __ldg(Mr + (size_t)(j + U + u) * n) : n;
 #pragma unroll
         for (int u = 0; u < U; u++) {
             T v[CB];
-            load_row<T, CB, VEC, LD_NC>(F + (size_t)idx[u] * B + c0, v);
+            load_row<T, CB, VEC, LD_NC>(Fc + (size_t)idx[u] * B, v);
 #pragma unroll
             for (int c = 0; c < CB; c++) acc[c] += v[c];
         }
-    }
-    for (; j < j1; j++) {
-        int32_t idx = ld_stream_i32(Mr + (size_t)j * n);
-        T v[CB];
-        load_row<T, CB, VEC, LD_NC>(F + (size_t)idx * B + c0, v);
 #pragma unroll
-        for (int c = 0; c < CB; c++) acc[c] += v[c];
+        for (int u = 0; u < U; u++) idx[u] = nidx[u];
     }
     T *dst;
     if (mode == 0)
@@ -446,6 +465,88 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, i
     else
         dst = out + ((size_t)slice * (row_hi - row_lo) + (r - row_lo)) * B + c0;
     store_row<T, CB, VEC>(dst, acc);
+}
+
+// Lanes over COLUMNS (B % 32 == 0): a warp owns TR consecutive ranks and 32
+// consecutive columns.  For chain j the TR indices M[j][r..r+TR-1] are
+// warp-uniform (staged in shared memory, KCH chains at a time, loaded one
+// chunk ahead through registers), so each DISTINCT row of F is fetched once
+// as one coalesced 256-B load and reused in registers for the run of ranks
+// that share it (chain-local posets: ~2-4 distinct rows per 16 ranks).  This
+// removes the L1 data-pipe bound of the lanes-over-ranks kernel, which
+// returns 8 B per (rank, chain, column) to every lane separately.
+template <typename T, int TR, int KCH>
+__global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restrict__ M, int32_t n,
+                                                     int32_t k, const T *__restrict__ F,
+                                                     T *__restrict__ out,
+                                                     const int32_t *__restrict__ rank_user,
+                                                     int64_t row_lo, int64_t row_hi, int32_t B,
+                                                     int G32, int mode) {
+    static_assert(KCH * TR == 32 * 32, "one chunk = 32 index words per lane");
+    __shared__ __align__(16) int32_t sidx[8][KCH][TR];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cg = (int)(blockIdx.x % G32);
+    const int64_t tile = blockIdx.x / G32;
+    const int64_t r0 = row_lo + (tile * 8 + warp) * TR;
+    if (r0 >= row_hi) return;
+    const int col = cg * 32 + lane;
+    const char *Fb = reinterpret_cast<const char *>(F + col);
+    const unsigned rowbytes = (unsigned)B * sizeof(T);
+    int32_t (*S)[TR] = sidx[warp];
+    // lane l loads words w = i*32 + l of the chunk: chain w / TR, rank w % TR
+    auto load_chunk = [&](int j0, int32_t (&reg)[32]) {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int w = i * 32 + lane, jj = w / TR, t = w % TR;
+            const int64_t r = r0 + t;
+            reg[i] = (j0 + jj < k && r < row_hi) ? __ldg(M + (size_t)(j0 + jj) * n + r) : n;
+        }
+    };
+    T acc[TR];
+#pragma unroll
+    for (int t = 0; t < TR; t++) acc[t] = T(0);
+    int32_t reg[32];
+    load_chunk(0, reg);
+    for (int j0 = 0; j0 < k; j0 += KCH) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int w = i * 32 + lane;
+            S[w / TR][w % TR] = reg[i];
+        }
+        __syncwarp();
+        if (j0 + KCH < k) load_chunk(j0 + KCH, reg);   // next chunk in flight during compute
+        const int jn = min(KCH, k - j0);
+        for (int jj = 0; jj < jn; jj++) {
+            int32_t id[TR];
+#pragma unroll
+            for (int t = 0; t < TR; t += 4) {
+                const int4 q = *reinterpret_cast<const int4 *>(&S[jj][t]);
+                id[t] = q.x; id[t + 1] = q.y; id[t + 2] = q.z; id[t + 3] = q.w;
+            }
+            // loads of the run heads only, all independent (no value chains
+            // through the loads), then the run values are forwarded by selects
+            u64 raw[TR];
+#pragma unroll
+            for (int t = 0; t < TR; t++)
+                raw[t] = ld_nc_if_ne(Fb + (size_t)(unsigned)id[t] * rowbytes, id[t],
+                                     t == 0 ? ~id[0] : id[t - 1]);
+            u64 v = raw[0];
+#pragma unroll
+            for (int t = 0; t < TR; t++) {
+                v = (t == 0 || id[t] != id[t - 1]) ? raw[t] : v;
+                acc[t] += from_bits<T>(v);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < TR; t++) {
+        const int64_t r = r0 + t;
+        if (r < row_hi) {
+            T *dst = mode == 0 ? out + (size_t)rank_user[r] * B : out + (size_t)(r - row_lo) * B;
+            dst[col] = acc[t];
+        }
+    }
 }
 
 template <typename T>
@@ -464,6 +565,12 @@ __global__ void k_gather_reduce(const T *__restrict__ part, T *__restrict__ out,
         out[(size_t)rr * B + b] = acc;
 }
 
+static int gather_cb(int64_t B) {
+    for (int cb : {8, 4, 2, 1})
+        if (B % cb == 0) return cb;
+    return 1;
+}
+
 static int pick_cb(int64_t B) {
     for (int cb : {32, 16, 8, 4, 2, 1})
         if (B % cb == 0) return cb;
@@ -471,7 +578,7 @@ static int pick_cb(int64_t B) {
 }
 
 static int gather_slices(const DevPoset &P, int64_t rows, int64_t B, int num_sms) {
-    int CB = pick_cb(B);
+    int CB = gather_cb(B);
     int64_t G = B / CB;
     int64_t warps = ((rows + 31) / 32) * G;
     int64_t target = (int64_t)num_sms * 48;
@@ -487,18 +594,22 @@ size_t gather_partial_bytes(const DevPoset &P, int64_t rows, int64_t B, int num_
 }
 
 template <typename T, int CB>
-static cudaError_t gather_cb(const DevPoset &P, const void *F, void *g, int64_t lo, int64_t hi,
-                             int64_t B, int mode, void *partial, int S, cudaStream_t s) {
+static cudaError_t gather_launch(const DevPoset &P, const void *F, void *g, int64_t lo, int64_t hi,
+                                 int64_t B, int mode, void *partial, int S, cudaStream_t s) {
     constexpr int VEC = (CB % 4 == 0) ? 4 : (CB % 2 == 0 ? 2 : 1);
-    constexpr int U = CB >= 32 ? 1 : (CB >= 16 ? 2 : (CB >= 8 ? 4 : 8));
+    constexpr int U = CB >= 8 ? 4 : (CB >= 4 ? 8 : 16);
     const int G = (int)(B / CB);
+    const int WG = (G % 4 == 0) ? 4 : (G % 2 == 0 ? 2 : 1);
+    const int GB = G / WG;
     const int64_t rows = hi - lo;
-    const int64_t tiles = (rows + 255) / 256;
-    const int64_t blocks = tiles * S * G;
+    const int64_t per_cta = 32 * (8 / WG);
+    const int64_t tiles = (rows + per_cta - 1) / per_cta;
+    const int64_t blocks = tiles * S * GB;
     void *dst = S > 1 ? partial : g;
     int m = S > 1 ? 2 : mode;
     k_gather<T, CB, VEC, U><<<(unsigned)blocks, 256, 0, s>>>(P.M, P.n, P.k, (const T *)F, (T *)dst,
-                                                             P.rank_user, lo, hi, (int32_t)B, G, S, m);
+                                                             P.rank_user, lo, hi, (int32_t)B, GB, WG,
+                                                             S, m);
     COUNT_LAUNCH(S > 1 ? 2 : 1);
     if (S > 1) {
         int64_t tot = rows * B;
@@ -513,13 +624,20 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
                             int64_t B, int mode, void *partial, int num_sms, cudaStream_t s) {
     int S = gather_slices(P, hi - lo, B, num_sms);
     if (S > 1 && !partial) S = 1;
-    switch (pick_cb(B)) {
-        case 32: return gather_cb<T, 32>(P, F, g, lo, hi, B, mode, partial, S, s);
-        case 16: return gather_cb<T, 16>(P, F, g, lo, hi, B, mode, partial, S, s);
-        case 8: return gather_cb<T, 8>(P, F, g, lo, hi, B, mode, partial, S, s);
-        case 4: return gather_cb<T, 4>(P, F, g, lo, hi, B, mode, partial, S, s);
-        case 2: return gather_cb<T, 2>(P, F, g, lo, hi, B, mode, partial, S, s);
-        default: return gather_cb<T, 1>(P, F, g, lo, hi, B, mode, partial, S, s);
+    if (B % 32 == 0 && S == 1) {
+        constexpr int TR = 16, KCH = 64;
+        const int G32 = (int)(B / 32);
+        const int64_t tiles = (hi - lo + 8 * TR - 1) / (8 * TR);
+        k_gather_cols<T, TR, KCH><<<(unsigned)(tiles * G32), 256, 0, s>>>(
+            P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+        COUNT_LAUNCH(1);
+        return cudaGetLastError();
+    }
+    switch (gather_cb(B)) {
+        case 8: return gather_launch<T, 8>(P, F, g, lo, hi, B, mode, partial, S, s);
+        case 4: return gather_launch<T, 4>(P, F, g, lo, hi, B, mode, partial, S, s);
+        case 2: return gather_launch<T, 2>(P, F, g, lo, hi, B, mode, partial, S, s);
+        default: return gather_launch<T, 1>(P, F, g, lo, hi, B, mode, partial, S, s);
     }
 }
 

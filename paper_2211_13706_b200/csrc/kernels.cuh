@@ -53,7 +53,7 @@ cudaError_t launch_gather(const DevPoset &P, int dtype, const void *F, void *g, 
                           int num_sms, cudaStream_t s);
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
-enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3 };
+enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4 };
 int moebius_pick(const DevPoset &P, int64_t batch, int max_level_width, int num_sms);
 cudaError_t launch_moebius_solve(const DevPoset &P, const int32_t *h_lvl_ptr, int dtype,
                                  const void *g, void *F, int64_t batch, int which,
@@ -66,5 +66,34 @@ cudaError_t launch_chain_diff(const DevPoset &P, int dtype, const void *F, void 
 // ---- g_user[user(r)] = g_rank[r] ----
 cudaError_t launch_rank_to_user(const DevPoset &P, int dtype, const void *g_rank, void *g_user,
                                 int64_t batch, cudaStream_t s);
+
+// ---- kernel (v), RING schedule (moebius_ring.cu) ----
+// Bounded-reach posets: U-solve + chain difference fused, one CTA per column,
+// F kept in a shared-memory ring, dependency rows streamed by bulk copies.
+struct RingPlan {
+    bool ok = false;
+    unsigned reach = 0;         // max rank distance to a dependency (incl. next)
+    int32_t kp = 0;             // padded row length of D (uint16 words): [next, chain 0..k-1, pad]
+    int32_t ring = 0;           // ring entries (power of two >= reach + max level width)
+    int32_t ch = 0, nstage = 0; // ranks per staged chunk, pipeline depth
+    int32_t threads = 0;        // CTA size
+    int32_t lpe = 1;            // lanes per element (1, 2, 4)
+    int64_t npad = 0;           // n rounded up to a multiple of ch
+    uint16_t *D = nullptr;      // [npad][kp]
+    int32_t *ru_pad = nullptr;  // [npad]
+};
+// Fills everything but the device pointers; ok = false if the poset does not
+// fit the schedule (reach >= 65535, rows or ring too large for shared memory).
+void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsigned reach,
+               RingPlan &R);
+size_t ring_smem_bytes(int ring, int kp, int ch, int nstage);
+cudaError_t launch_reach_max(const DevPoset &P, const int32_t *slot_rank, unsigned *out,
+                             cudaStream_t s);
+cudaError_t launch_build_dist(const DevPoset &P, const int32_t *slot_rank, int32_t kp, int32_t ring,
+                              int64_t npad, uint16_t *D, cudaStream_t s);
+cudaError_t launch_to_rank_major(const DevPoset &P, int dtype, const void *g, int64_t B,
+                                 int64_t npad, void *gP, cudaStream_t s);
+cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype, const void *gP,
+                                void *f, int64_t B, cudaStream_t s);
 
 }  // namespace poset

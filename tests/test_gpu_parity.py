@@ -2,7 +2,7 @@
 
 Bar (BASELINE.json north star): int64 bit-exact (Z/2^64); fp64 within
 |Δ| <= 1e-9 * Σ_{y⪯x}|f(y)| (scale computed by the oracle).  Möbius fp64 is
-only compared where μ is bounded (Boolean lattice, shallow posets; reading R8
+only compared where μ is bounded (Boolean lattice, shallow posets; reading G8
 of DESIGN.md); deep posets use int64 round trips.
 """
 import numpy as np
@@ -21,7 +21,13 @@ import paper_2211_13706_b200 as pz  # noqa: E402
 from oracle import brute  # noqa: E402
 from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
 
-KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP]
+KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING]
+
+
+def kernels_for(P):
+    """Every Möbius schedule that applies to P (RING needs a bounded reach)."""
+    ring_ok = P.info()["dist_bytes"] > 0
+    return [k for k in KERNELS if k != pz.MOEB_RING or ring_ok]
 facts = load_facts()
 PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
 
@@ -66,7 +72,7 @@ def test_example_paper_N_and_transforms(paper_example):
     Z, M = load_matrix("Z.txt"), load_matrix("M.txt")
     f = W.int_values(12, 5, -100, 100, seed=3)
     assert (gpu_zeta(P, f) == Z @ f).all()
-    for kern in KERNELS:
+    for kern in kernels_for(P):
         assert (gpu_moebius(P, f, kern) == M @ f).all()
     ff = W.normal_values(12, 4, seed=4)
     assert_fp64_close(gpu_zeta(P, ff), Z @ ff, Z @ np.abs(ff))
@@ -140,7 +146,7 @@ def test_int64_zeta_moebius_vs_O2(inst, B, built):
     f = W.int_values(n, B, -1000, 1000, seed=B)
     g = gpu_zeta(P, f)
     assert (g == O.zeta(f)).all()
-    for kern in KERNELS:
+    for kern in kernels_for(P):
         if kern == pz.MOEB_LEVEL and P.ell > 3000:
             continue
         assert (gpu_moebius(P, g, kern) == f).all(), kern
@@ -164,13 +170,13 @@ def test_fp64_zeta_vs_O2(inst, B, built):
     ("C4w_24L", 24 * 256, lambda: W.layered_dag(24, 256, 3, 0, forced=True)),
 ])
 def test_fp64_moebius_shallow_vs_O2(name, n, make):
-    """fp64 Möbius only where |μ| stays small (reading R8)."""
+    """fp64 Möbius only where |μ| stays small (reading G8)."""
     src, dst = make()
     P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
     f = W.normal_values(n, 2, seed=3)
     g = O.zeta(f)
     want = O.moebius(g)
-    for kern in KERNELS:
+    for kern in kernels_for(P):
         assert_fp64_close(gpu_moebius(P, g, kern), want, O.zeta(np.abs(want)))
 
 
@@ -187,13 +193,38 @@ def test_C2_boolean_lattice_vs_yates():
     g = gpu_zeta(P, f)
     assert_fp64_close(g, brute.yates_zeta(bits, f), brute.yates_zeta(bits, np.abs(f)))
     gy = brute.yates_zeta(bits, f)
-    for kern in KERNELS:
+    for kern in kernels_for(P):
         assert_fp64_close(gpu_moebius(P, gy, kern), brute.yates_moebius(bits, gy),
                           brute.yates_zeta(bits, np.abs(f)))
     fi = W.int_values(n, 2, -1000, 1000, seed=2)
     gi = gpu_zeta(P, fi)
     assert (gi == brute.yates_zeta(bits, fi)).all()
     assert (gpu_moebius(P, gi) == fi).all()
+
+
+# ------------------------------------------------------- RING schedule
+
+def test_ring_schedule_selection_and_limits():
+    """RING is chosen for bounded-reach posets, refused where it cannot run."""
+    n = 20000
+    src, dst = W.window_dag(n, 2, 64, 3, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    info = P.info()
+    assert info["dist_bytes"] > 0 and 0 < info["reach"] < 65535
+    assert info["moebius_kernel"] == pz.MOEB_RING
+    for B in (1, 2, 7, 33):
+        f = W.int_values(n, B, -1000, 1000, seed=B)
+        g = gpu_zeta(P, f)
+        assert (gpu_moebius(P, g) == f).all(), B
+        h = W.int_values(n, B, -10**17, 10**17, seed=B + 9)
+        assert (gpu_moebius(P, h, pz.MOEB_RING) == O.moebius(h)).all(), B
+    # wide levels (Boolean lattice 2^12: 924-element middle level) do not fit
+    Pb = pz.Poset(4096, *W.boolean_lattice(12))
+    assert Pb.info()["dist_bytes"] == 0
+    Pb.set_option("moebius_kernel", pz.MOEB_RING)
+    with pytest.raises(pz.PosetError) as e:
+        Pb.moebius(dev(np.zeros((4096, 1), np.int64)))
+    assert e.value.code == "EINVAL"
 
 
 # ---------------------------------------------------------------- edge cases

@@ -276,7 +276,7 @@ def make_workload(name: str, scale: float = 1.0, dtype: str | None = None,
                   batch: int | None = None) -> Workload:
     """Build config ``name`` at ``scale`` (n multiplied by scale; C2 halves
     the bit count per factor 2).  ``dtype``/``batch`` override the config's
-    (e.g. int64 round-trip parity on C5w, reading R8)."""
+    (e.g. int64 round-trip parity on C5w, reading G8)."""
     builder, B, dt, rng_, desc = CONFIGS[name]
     n, src, dst = builder(scale)
     dt = dtype or dt
