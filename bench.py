@@ -38,7 +38,7 @@ PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
                 "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
                 "chain_diff": "k_chain_diff"}
-MOEB_NAMES = ["auto", "level", "grid", "warp", "ring"]
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr"]
 
 
 def parse():
@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--dtype", default=None, choices=[None, "i64", "f64"])
     ap.add_argument("--batch", type=int, default=None, help="functions per rank")
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--moebius-kernel", default="auto", choices=["auto", "level", "grid", "warp", "ring"])
+    ap.add_argument("--moebius-kernel", default="auto", choices=MOEB_NAMES)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -71,8 +71,10 @@ typedef enum {
     POSET_MOEB_LEVEL = 1,     /* one launch per antichain level (Alg. 5)     */
     POSET_MOEB_GRID = 2,      /* persistent cooperative kernel, grid barrier per level   */
     POSET_MOEB_WARP = 3,      /* one warp per column group sweeps all levels (no grid sync) */
-    POSET_MOEB_RING = 4       /* bounded-reach posets: one CTA per column, F in a shared-memory
+    POSET_MOEB_RING = 4,      /* bounded-reach posets: one CTA per column, F in a shared-memory
                                  ring, U-solve and chain difference fused   */
+    POSET_MOEB_CSR = 5        /* sparse U-rows, persistent kernel with a grid barrier per
+                                 level, one warp per (element, column group) */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -95,7 +97,9 @@ typedef struct {
     int64_t reach;        /* max rank distance from x to a dependency of its U-solve
                              row or to next(x) (level order); RING needs < 65535     */
     int64_t dist_bytes;   /* bytes of the RING distance table (0 = RING unavailable)*/
-    double t_dist;        /* seconds: reach + distance table build                  */
+    double t_dist;        /* seconds: reach + distance table + sparse rows build    */
+    int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
+    int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
 } poset_info;
 
 /*

@@ -37,6 +37,8 @@ struct poset_s {
     unsigned *d_bar = nullptr;
     unsigned long long *d_count = nullptr;
     RingPlan ring;                    // RING Möbius schedule (moebius_ring.cu)
+    CsrRows csr;                      // sparse U-rows (moebius_csr.cu)
+    bool zeta_csr = false;            // zeta gathers over the CSR rows (sparse table)
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
     size_t gP_bytes = 0;
     // scratch, grown on demand
@@ -88,7 +90,7 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.ru_pad, h->d_gP};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->d_gP, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -155,17 +157,21 @@ static poset_status finish_setup(poset_s *h) {
             size_t dbytes = (size_t)h->ring.npad * h->ring.kp * 2;
             size_t fb = 0, tb = 0;
             cudaMemGetInfo(&fb, &tb);
-            if (dbytes + (size_t)h->ring.npad * 4 + ((size_t)1 << 30) > fb ||
+            if (dbytes + (size_t)h->ring.npad * 6 + ((size_t)1 << 30) > fb ||
                 cudaMalloc((void **)&h->ring.D, dbytes) != cudaSuccess ||
+                cudaMalloc((void **)&h->ring.Pn, (size_t)h->ring.npad * 2) != cudaSuccess ||
                 cudaMalloc((void **)&h->ring.ru_pad, (size_t)h->ring.npad * 4) != cudaSuccess) {
                 cudaGetLastError();
                 if (h->ring.D) cudaFree(h->ring.D);
+                if (h->ring.Pn) cudaFree(h->ring.Pn);
                 h->ring.D = nullptr;
+                h->ring.Pn = nullptr;
                 h->ring.ok = false;
             }
         }
         if (h->ring.ok) {
-            e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, h->ring.npad, h->ring.D, 0);
+            e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, h->ring.npad, h->ring.D,
+                                  h->ring.Pn, 0);
             if (e == cudaSuccess) e = cudaMemset(h->ring.ru_pad, 0, (size_t)h->ring.npad * 4);
             if (e == cudaSuccess)
                 e = cudaMemcpy(h->ring.ru_pad, h->d_rank_user, (size_t)H.n * 4, cudaMemcpyDeviceToDevice);
@@ -173,6 +179,18 @@ static poset_status finish_setup(poset_s *h) {
             if (e != cudaSuccess) { cudaFree(d_slot_rank); CK(e); }
         }
         CK(cudaFree(d_slot_rank));
+    }
+    // sparse U-rows: for the Möbius solve when RING does not apply, and for
+    // the zeta gather when the dense table is mostly ∞ (fill < 1/2)
+    {
+        const double fill = H.n && H.k ? (double)nnz / ((double)H.n * H.k) : 1.0;
+        if (!h->ring.ok || fill < 0.5) {
+            size_t fb = 0, tb = 0;
+            CK(cudaMemGetInfo(&fb, &tb));
+            const size_t reserve = (size_t)1 << 30;
+            CK(build_csr(P, h->csr, fb > reserve ? fb - reserve : 0));
+            h->zeta_csr = h->csr.ok && fill < 0.5;
+        }
     }
     double t3 = now_seconds();
     poset_info &I = h->info;
@@ -191,9 +209,13 @@ static poset_status finish_setup(poset_s *h) {
     I.t_mtable = t2 - t1;
     I.device = h->device;
     I.reach = h->ring.reach;
-    I.dist_bytes = h->ring.ok ? (int64_t)h->ring.npad * h->ring.kp * 2 : 0;
+    I.dist_bytes = h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0;
     I.t_dist = t3 - t2;
-    I.moebius_kernel = h->ring.ok ? MOEB_RING : moebius_pick(P, 1, H.max_level_width, h->num_sms);
+    I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
+    I.zeta_sparse = h->zeta_csr ? 1 : 0;
+    I.moebius_kernel = h->ring.ok  ? MOEB_RING
+                       : h->csr.ok ? MOEB_CSR
+                                   : moebius_pick(P, 1, H.max_level_width, h->num_sms);
     // drop host arrays only the device needs
     std::vector<int32_t>().swap(H.child);
     std::vector<int64_t>().swap(H.child_ptr);
@@ -340,7 +362,10 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
     }
     {
         PhaseTimer t(h, POSET_PH_GATHER, s);
-        CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, h->num_sms, s));
+        if (h->zeta_csr)
+            CK(launch_gather_csr(P, h->csr, dt, h->d_F, g, 0, h->H.n, B, 0, s));
+        else
+            CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, h->num_sms, s));
     }
     return POSET_OK;
 }
@@ -351,7 +376,16 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
     DevPoset P = h->dev();
     int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
                 : h->ring.ok ? MOEB_RING
+                : h->csr.ok  ? MOEB_CSR
                              : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+    if (which == MOEB_CSR) {
+        if (!h->csr.ok)
+            return fail(POSET_EINVAL, "poset_moebius: the CSR schedule has no sparse rows for this "
+                                      "poset (not built: RING applies or memory); use AUTO");
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_csr(P, h->csr, dt, g, h->d_F, f, B, h->d_bar, h->num_sms, s));
+        return POSET_OK;
+    }
     h->info.moebius_kernel = which;
     if (which == MOEB_RING) {
         if (!h->ring.ok)
@@ -459,6 +493,10 @@ poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t l
     if (st) return st;
     if (lo < 0 || hi > h->H.n || lo > hi) return fail(POSET_EINVAL, "poset_gather_rows: bad range");
     CK(cudaSetDevice(h->device));
+    if (h->zeta_csr) {
+        CK(launch_gather_csr(h->dev(), h->csr, dt, F, g_rank, lo, hi, batch, 1, (cudaStream_t)stream));
+        return POSET_OK;
+    }
     size_t pb = gather_partial_bytes(h->dev(), hi - lo, batch, h->num_sms);
     if (pb) {
         st = grow(h, &h->d_part, &h->part_bytes, pb);
@@ -535,8 +573,17 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_RING) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_CSR) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
+        return POSET_OK;
+    }
+    if (!strcmp(key, "ring_lpe")) {   // lanes per element of the RING schedule (tuning)
+        const int64_t E = h->ring.entries ? h->ring.entries / value : 0;
+        if (!h->ring.ok || value < 1 || value > 32 || (value & (value - 1)) || E < 4 || E > 64 ||
+            (E == 4 && value < 16))
+            return fail(POSET_EINVAL, "poset_set_option: ring_lpe must be a power of two with "
+                                      "4 <= entries/ring_lpe <= 64");
+        h->ring.lpe = (int32_t)value;
         return POSET_OK;
     }
     if (!strcmp(key, "profile")) {

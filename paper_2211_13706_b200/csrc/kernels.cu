@@ -111,18 +111,6 @@ __device__ __forceinline__ void store_row(T *p, const T (&o)[CB]) {
 
 __device__ __forceinline__ int32_t ld_stream_i32(const int32_t *p) { return __ldcs(p); }
 
-// 8-byte read-only load issued only if a != b; the result register is left
-// undefined otherwise.  Opaque to the compiler on purpose: it keeps the
-// predicated loads of a run independent of each other (the C++ form gets
-// rewritten into a chain "dst = previous value; @p ld dst").
-__device__ __forceinline__ u64 ld_nc_if_ne(const void *p, int32_t a, int32_t b) {
-    u64 v;
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, %3;\n\t@q ld.global.nc.b64 %0, [%1];\n\t}"
-        : "=l"(v)
-        : "l"(p), "r"(a), "r"(b));
-    return v;
-}
-
 // ---------------------------------------------------- (ii) m-table build --
 // One warp per chain j.  For every level L (bottom-up) and every rank r of L:
 //   M[j][r] = slot(r)                               if chain(r) == j
@@ -467,23 +455,54 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, i
     store_row<T, CB, VEC>(dst, acc);
 }
 
-// Lanes over COLUMNS (B % 32 == 0): a warp owns TR consecutive ranks and 32
-// consecutive columns.  For chain j the TR indices M[j][r..r+TR-1] are
-// warp-uniform (staged in shared memory, KCH chains at a time, loaded one
-// chunk ahead through registers), so each DISTINCT row of F is fetched once
-// as one coalesced 256-B load and reused in registers for the run of ranks
-// that share it (chain-local posets: ~2-4 distinct rows per 16 ranks).  This
-// removes the L1 data-pipe bound of the lanes-over-ranks kernel, which
-// returns 8 B per (rank, chain, column) to every lane separately.
-template <typename T, int TR, int KCH>
+// Lanes over COLUMNS (B % 32 == 0): a warp owns TR = 8 consecutive ranks and
+// 32 consecutive columns.  For chain j the 8 indices M[j][r..r+7] are
+// warp-uniform; each DISTINCT row of F among them (a "run head") is fetched
+// once as one coalesced 256-B load and forwarded in registers to the rest of
+// its run (chain-local posets: 1-3 distinct rows per 8 ranks).  This removes
+// the L1 data-pipe bound of the lanes-over-ranks kernel (8 B returned to every
+// lane per rank, chain and column).  Index chunks (KCH chains x 8 ranks) are
+// staged in shared memory by cp.async one chunk ahead; the row loads of chain
+// j+1 are issued before chain j is resolved (software pipeline).
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// raw[t] = *(row of id[t]) if id[t] starts a run (t == 0 or id[t] != id[t-1]),
+// undefined otherwise; one asm block so the 8 loads stay independent.
+__device__ __forceinline__ void head_loads8(const char *Fb, unsigned rowbytes, const int32_t (&id)[8],
+                                           u64 (&raw)[8]) {
+    const char *p[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) p[t] = Fb + (size_t)(unsigned)id[t] * rowbytes;
+    asm("{\n\t.reg .pred q<8>;\n\t"
+        "setp.ne.s32 q1, %9, %8;\n\tsetp.ne.s32 q2, %10, %9;\n\tsetp.ne.s32 q3, %11, %10;\n\t"
+        "setp.ne.s32 q4, %12, %11;\n\tsetp.ne.s32 q5, %13, %12;\n\tsetp.ne.s32 q6, %14, %13;\n\t"
+        "setp.ne.s32 q7, %15, %14;\n\t"
+        "ld.global.nc.b64 %0, [%16];\n\t"
+        "@q1 ld.global.nc.b64 %1, [%17];\n\t@q2 ld.global.nc.b64 %2, [%18];\n\t"
+        "@q3 ld.global.nc.b64 %3, [%19];\n\t@q4 ld.global.nc.b64 %4, [%20];\n\t"
+        "@q5 ld.global.nc.b64 %5, [%21];\n\t@q6 ld.global.nc.b64 %6, [%22];\n\t"
+        "@q7 ld.global.nc.b64 %7, [%23];\n\t}"
+        : "=l"(raw[0]), "=l"(raw[1]), "=l"(raw[2]), "=l"(raw[3]), "=l"(raw[4]), "=l"(raw[5]),
+          "=l"(raw[6]), "=l"(raw[7])
+        : "r"(id[0]), "r"(id[1]), "r"(id[2]), "r"(id[3]), "r"(id[4]), "r"(id[5]), "r"(id[6]),
+          "r"(id[7]), "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]), "l"(p[4]), "l"(p[5]), "l"(p[6]),
+          "l"(p[7]));
+}
+
+template <typename T, int KCH>
 __global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restrict__ M, int32_t n,
-                                                     int32_t k, const T *__restrict__ F,
-                                                     T *__restrict__ out,
-                                                     const int32_t *__restrict__ rank_user,
-                                                     int64_t row_lo, int64_t row_hi, int32_t B,
-                                                     int G32, int mode) {
-    static_assert(KCH * TR == 32 * 32, "one chunk = 32 index words per lane");
-    __shared__ __align__(16) int32_t sidx[8][KCH][TR];
+                                                        int32_t k, const T *__restrict__ F,
+                                                        T *__restrict__ out,
+                                                        const int32_t *__restrict__ rank_user,
+                                                        int64_t row_lo, int64_t row_hi, int32_t B,
+                                                        int G32, int mode) {
+    constexpr int TR = 8;
+    __shared__ __align__(16) int32_t sidx[2][8][KCH][TR];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cg = (int)(blockIdx.x % G32);
     const int64_t tile = blockIdx.x / G32;
@@ -492,52 +511,59 @@ __global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restric
     const int col = cg * 32 + lane;
     const char *Fb = reinterpret_cast<const char *>(F + col);
     const unsigned rowbytes = (unsigned)B * sizeof(T);
-    int32_t (*S)[TR] = sidx[warp];
-    // lane l loads words w = i*32 + l of the chunk: chain w / TR, rank w % TR
-    auto load_chunk = [&](int j0, int32_t (&reg)[32]) {
-#pragma unroll
-        for (int i = 0; i < 32; i++) {
+    const int nchunk = (k + KCH - 1) / KCH;
+    // word w of a chunk (KCH*TR words, KCH*TR/32 per lane): chain w / TR, rank w % TR
+    auto stage = [&](int c) {
+        int32_t (*S)[TR] = sidx[c & 1][warp];
+        const int j0 = c * KCH;
+#pragma unroll 4
+        for (int i = 0; i < KCH * TR / 32; i++) {
             const int w = i * 32 + lane, jj = w / TR, t = w % TR;
             const int64_t r = r0 + t;
-            reg[i] = (j0 + jj < k && r < row_hi) ? __ldg(M + (size_t)(j0 + jj) * n + r) : n;
+            if (j0 + jj < k && r < row_hi)
+                cp_async4(&S[jj][t], M + (size_t)(j0 + jj) * n + r);
+            else
+                S[jj][t] = n;   // the zero row of F
         }
     };
     T acc[TR];
 #pragma unroll
     for (int t = 0; t < TR; t++) acc[t] = T(0);
-    int32_t reg[32];
-    load_chunk(0, reg);
-    for (int j0 = 0; j0 < k; j0 += KCH) {
+    stage(0);
+    for (int c = 0; c < nchunk; c++) {
+        cp_async_wait_all();
         __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 32; i++) {
-            const int w = i * 32 + lane;
-            S[w / TR][w % TR] = reg[i];
-        }
-        __syncwarp();
-        if (j0 + KCH < k) load_chunk(j0 + KCH, reg);   // next chunk in flight during compute
-        const int jn = min(KCH, k - j0);
-        for (int jj = 0; jj < jn; jj++) {
-            int32_t id[TR];
-#pragma unroll
-            for (int t = 0; t < TR; t += 4) {
-                const int4 q = *reinterpret_cast<const int4 *>(&S[jj][t]);
-                id[t] = q.x; id[t + 1] = q.y; id[t + 2] = q.z; id[t + 3] = q.w;
-            }
-            // loads of the run heads only, all independent (no value chains
-            // through the loads), then the run values are forwarded by selects
-            u64 raw[TR];
-#pragma unroll
-            for (int t = 0; t < TR; t++)
-                raw[t] = ld_nc_if_ne(Fb + (size_t)(unsigned)id[t] * rowbytes, id[t],
-                                     t == 0 ? ~id[0] : id[t - 1]);
+        if (c + 1 < nchunk) stage(c + 1);   // next chunk in flight during this one
+        int32_t (*S)[TR] = sidx[c & 1][warp];
+        const int jn = min(KCH, k - c * KCH);
+        // ping-pong register sets A / B: the loads of one chain are in flight
+        // while the other chain is resolved (no register moves between them)
+        int32_t idA[TR], idB[TR];
+        u64 rawA[TR], rawB[TR];
+        auto fetch = [&](int jj, int32_t (&id)[TR], u64 (&raw)[TR]) {
+            const int4 q0 = *reinterpret_cast<const int4 *>(&S[jj][0]);
+            const int4 q1 = *reinterpret_cast<const int4 *>(&S[jj][4]);
+            id[0] = q0.x; id[1] = q0.y; id[2] = q0.z; id[3] = q0.w;
+            id[4] = q1.x; id[5] = q1.y; id[6] = q1.z; id[7] = q1.w;
+            head_loads8(Fb, rowbytes, id, raw);
+        };
+        auto resolve = [&](const int32_t (&id)[TR], const u64 (&raw)[TR]) {
             u64 v = raw[0];
 #pragma unroll
             for (int t = 0; t < TR; t++) {
-                v = (t == 0 || id[t] != id[t - 1]) ? raw[t] : v;
+                if (t > 0) v = id[t] != id[t - 1] ? raw[t] : v;
                 acc[t] += from_bits<T>(v);
             }
+        };
+        fetch(0, idA, rawA);
+#pragma unroll 1
+        for (int jj = 0; jj < jn; jj += 2) {
+            if (jj + 1 < jn) fetch(jj + 1, idB, rawB);
+            resolve(idA, rawA);
+            if (jj + 2 < jn) fetch(jj + 2, idA, rawA);
+            if (jj + 1 < jn) resolve(idB, rawB);
         }
+        __syncwarp();
     }
 #pragma unroll
     for (int t = 0; t < TR; t++) {
@@ -625,10 +651,10 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
     int S = gather_slices(P, hi - lo, B, num_sms);
     if (S > 1 && !partial) S = 1;
     if (B % 32 == 0 && S == 1) {
-        constexpr int TR = 16, KCH = 64;
+        constexpr int TR = 8, KCH = 64;
         const int G32 = (int)(B / 32);
         const int64_t tiles = (hi - lo + 8 * TR - 1) / (8 * TR);
-        k_gather_cols<T, TR, KCH><<<(unsigned)(tiles * G32), 256, 0, s>>>(
+        k_gather_cols<T, KCH><<<(unsigned)(tiles * G32), 256, 0, s>>>(
             P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         COUNT_LAUNCH(1);
         return cudaGetLastError();

@@ -53,7 +53,7 @@ cudaError_t launch_gather(const DevPoset &P, int dtype, const void *F, void *g, 
                           int num_sms, cudaStream_t s);
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
-enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4 };
+enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5 };
 int moebius_pick(const DevPoset &P, int64_t batch, int max_level_width, int num_sms);
 cudaError_t launch_moebius_solve(const DevPoset &P, const int32_t *h_lvl_ptr, int dtype,
                                  const void *g, void *F, int64_t batch, int which,
@@ -73,13 +73,14 @@ cudaError_t launch_rank_to_user(const DevPoset &P, int dtype, const void *g_rank
 struct RingPlan {
     bool ok = false;
     unsigned reach = 0;         // max rank distance to a dependency (incl. next)
-    int32_t kp = 0;             // padded row length of D (uint16 words): [next, chain 0..k-1, pad]
+    int32_t kp = 0;             // padded row length of D (uint16 words): entries + 8
     int32_t ring = 0;           // ring entries (power of two >= reach + max level width)
     int32_t ch = 0, nstage = 0; // ranks per staged chunk, pipeline depth
-    int32_t threads = 0;        // CTA size
-    int32_t lpe = 1;            // lanes per element (1, 2, 4)
+    int32_t entries = 0;        // row entries (64, 128 or 256 >= k)
+    int32_t lpe = 1;            // lanes per element; entries / lpe per lane (8..64)
     int64_t npad = 0;           // n rounded up to a multiple of ch
     uint16_t *D = nullptr;      // [npad][kp]
+    uint16_t *Pn = nullptr;     // [npad] ring slot of next(r)
     int32_t *ru_pad = nullptr;  // [npad]
 };
 // Fills everything but the device pointers; ok = false if the poset does not
@@ -90,10 +91,27 @@ size_t ring_smem_bytes(int ring, int kp, int ch, int nstage);
 cudaError_t launch_reach_max(const DevPoset &P, const int32_t *slot_rank, unsigned *out,
                              cudaStream_t s);
 cudaError_t launch_build_dist(const DevPoset &P, const int32_t *slot_rank, int32_t kp, int32_t ring,
-                              int64_t npad, uint16_t *D, cudaStream_t s);
+                              int64_t npad, uint16_t *D, uint16_t *Pn, cudaStream_t s);
 cudaError_t launch_to_rank_major(const DevPoset &P, int dtype, const void *g, int64_t B,
                                  int64_t npad, void *gP, cudaStream_t s);
 cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype, const void *gP,
                                 void *f, int64_t B, cudaStream_t s);
+
+// ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----
+struct CsrRows {
+    bool ok = false;
+    int64_t nnz = 0;            // entries (U-rows: niv_j(r), j ≠ id(r), ∞ omitted)
+    int64_t *ptr = nullptr;     // [n+1] rank order
+    int32_t *idx = nullptr;     // [nnz] F slots
+};
+// Builds the rows from the dense table if they fit in free_budget bytes
+// (C.ok = false otherwise; not an error).
+cudaError_t build_csr(const DevPoset &P, CsrRows &C, size_t free_budget);
+cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *F,
+                              void *g, int64_t row_lo, int64_t row_hi, int64_t batch,
+                              int out_rank, cudaStream_t s);
+cudaError_t launch_moebius_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *g,
+                               void *F, void *f, int64_t batch, unsigned *barrier, int num_sms,
+                               cudaStream_t s);
 
 }  // namespace poset

@@ -1,0 +1,295 @@
+// Sparse (CSR) niv rows -- SURVEY.md §8(f) N1 -- and the two kernels that use
+// them:
+//
+//   U-rows   for rank r: the F slots of niv_j(r) for j ≠ id(r), ∞ omitted
+//            (the paper stores N sparse with ∞ dropped, and drops the
+//            self entries in practice, P:L582 / P:L670).  int32 slots,
+//            int64 row pointers, rank order.  Built from the dense table M.
+//
+//   k_gather_csr   zeta, Eq. zeta-fast:
+//                  g(x) = F[slot(x)] + Σ_{s ∈ U-row(x)} F[s]
+//                  (the self entry is niv_{id(x)}(x) = x).
+//   k_moeb_csr     Möbius, Alg. 4: persistent cooperative
+//                  kernel, one grid barrier per antichain level (Alg. 5,
+//                  P:L692-705); warp-granular items, so wide rows (large k)
+//                  are summed by 32 lanes in parallel instead of one thread:
+//                    F(x) = g(x) - Σ_{s ∈ U-row(x)} F[s];  f(x) = F(x) - F(next(x))
+//
+// Two lane mappings: lanes over the row's entries (B < 32, one column at a
+// time, warp-shuffle reduction) or lanes over columns (B % 32 == 0; each row
+// entry is read once by the warp and broadcast by a shuffle, the F row is one
+// coalesced 256-B load).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace poset {
+
+typedef unsigned long long u64;
+
+// ------------------------------------------------------------ build ------
+__global__ void k_csr_count(const int32_t *__restrict__ M, int32_t n, int32_t k,
+                            const int32_t *__restrict__ chain, int32_t *__restrict__ cnt) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int32_t own = chain[r];
+    int32_t c = 0;
+    for (int32_t j = 0; j < k; j++) c += (j != own) & (__ldcs(M + (size_t)j * n + r) != n);
+    cnt[r] = c;
+}
+
+__global__ void k_csr_fill(const int32_t *__restrict__ M, int32_t n, int32_t k,
+                           const int32_t *__restrict__ chain, const int64_t *__restrict__ ptr,
+                           int32_t *__restrict__ idx) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int32_t own = chain[r];
+    int64_t o = ptr[r];
+    for (int32_t j = 0; j < k; j++) {
+        const int32_t s = __ldcs(M + (size_t)j * n + r);
+        if (j != own && s != n) idx[o++] = s;
+    }
+}
+
+cudaError_t build_csr(const DevPoset &P, CsrRows &C, size_t free_budget) {
+    C.ok = false;
+    const int32_t n = P.n;
+    if (n == 0) return cudaSuccess;
+    int32_t *d_cnt = nullptr;
+    cudaError_t e = cudaMalloc((void **)&d_cnt, (size_t)n * 4);
+    if (e != cudaSuccess) return e;
+    k_csr_count<<<(n + 255) / 256, 256>>>(P.M, n, P.k, P.chain, d_cnt);
+    launches_add(1);
+    std::vector<int32_t> cnt((size_t)n);
+    e = cudaMemcpy(cnt.data(), d_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(d_cnt);
+    if (e != cudaSuccess) return e;
+    std::vector<int64_t> ptr((size_t)n + 1, 0);
+    for (int32_t r = 0; r < n; r++) ptr[r + 1] = ptr[r] + cnt[r];
+    C.nnz = ptr[n];
+    const size_t bytes = (size_t)std::max<int64_t>(C.nnz, 1) * 4 + ((size_t)n + 1) * 8;
+    if (bytes > free_budget) return cudaSuccess;   // not enough room: no CSR rows
+    e = cudaMalloc((void **)&C.ptr, ((size_t)n + 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&C.idx, (size_t)std::max<int64_t>(C.nnz, 1) * 4);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (C.ptr) cudaFree(C.ptr);
+        C.ptr = nullptr;
+        C.idx = nullptr;
+        return cudaSuccess;
+    }
+    e = cudaMemcpy(C.ptr, ptr.data(), ((size_t)n + 1) * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    k_csr_fill<<<(n + 255) / 256, 256>>>(P.M, n, P.k, P.chain, C.ptr, C.idx);
+    launches_add(1);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+    C.ok = true;
+    return cudaSuccess;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_cg(const T *p);
+template <>
+__device__ __forceinline__ double ld_cg<double>(const double *p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ u64 ld_cg<u64>(const u64 *p) { return __ldcg(p); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + c] by one warp, lanes over entries; the
+// result is valid in every lane.  LOAD: plain (read-only data) or .cg (data
+// written earlier in the same kernel by other SMs).
+template <typename T, bool CG>
+__device__ __forceinline__ T row_sum_lanes(const int32_t *__restrict__ idx, int64_t a, int64_t b,
+                                           const T *Fsrc, int32_t B, int c) {
+    const int lane = threadIdx.x & 31;
+    T s0 = T(0), s1 = T(0);
+    int64_t e = a + lane;
+    for (; e + 32 < b; e += 64) {
+        const int32_t i0 = __ldg(idx + e), i1 = __ldg(idx + e + 32);
+        const T *p0 = Fsrc + (size_t)i0 * B + c, *p1 = Fsrc + (size_t)i1 * B + c;
+        s0 += CG ? ld_cg(p0) : __ldg(p0);
+        s1 += CG ? ld_cg(p1) : __ldg(p1);
+    }
+    if (e < b) {
+        const T *p0 = Fsrc + (size_t)__ldg(idx + e) * B + c;
+        s0 += CG ? ld_cg(p0) : __ldg(p0);
+    }
+    return warp_sum(s0 + s1);
+}
+
+// Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + col] by one warp, lanes over columns.
+template <typename T, bool CG>
+__device__ __forceinline__ T row_sum_cols(const int32_t *__restrict__ idx, int64_t a, int64_t b,
+                                          const T *Fsrc, int32_t B, int col) {
+    const int lane = threadIdx.x & 31;
+    T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+    for (int64_t e0 = a; e0 < b; e0 += 32) {
+        const int m = (int)(b - e0 < 32 ? b - e0 : 32);
+        const int32_t mine = lane < m ? __ldg(idx + e0 + lane) : 0;
+        int q = 0;
+        for (; q + 4 <= m; q += 4) {
+            const int32_t i0 = __shfl_sync(0xffffffffu, mine, q);
+            const int32_t i1 = __shfl_sync(0xffffffffu, mine, q + 1);
+            const int32_t i2 = __shfl_sync(0xffffffffu, mine, q + 2);
+            const int32_t i3 = __shfl_sync(0xffffffffu, mine, q + 3);
+            const T *p0 = Fsrc + (size_t)i0 * B + col, *p1 = Fsrc + (size_t)i1 * B + col;
+            const T *p2 = Fsrc + (size_t)i2 * B + col, *p3 = Fsrc + (size_t)i3 * B + col;
+            s0 += CG ? ld_cg(p0) : __ldg(p0);
+            s1 += CG ? ld_cg(p1) : __ldg(p1);
+            s2 += CG ? ld_cg(p2) : __ldg(p2);
+            s3 += CG ? ld_cg(p3) : __ldg(p3);
+        }
+        for (; q < m; q++) {
+            const int32_t i0 = __shfl_sync(0xffffffffu, mine, q);
+            const T *p0 = Fsrc + (size_t)i0 * B + col;
+            s0 += CG ? ld_cg(p0) : __ldg(p0);
+        }
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
+// ---------------------------------------------------- zeta gather (CSR) ---
+// One warp per (rank, 32-column group) [COLS] or per rank [lanes over entries].
+template <typename T, bool COLS>
+__global__ void __launch_bounds__(256) k_gather_csr(DevPoset P, const int64_t *__restrict__ ptr,
+                                                    const int32_t *__restrict__ idx,
+                                                    const T *__restrict__ F, T *__restrict__ out,
+                                                    int64_t row_lo, int64_t row_hi, int32_t B,
+                                                    int G, int mode) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t items = (row_hi - row_lo) * G;
+    if (w >= items) return;
+    const int64_t r = row_lo + w / G;
+    const int cg = (int)(w % G);
+    const int64_t a = ptr[r], b = ptr[r + 1];
+    const int32_t my = P.slot[r];
+    T *dst = mode == 0 ? out + (size_t)P.rank_user[r] * B : out + (size_t)(r - row_lo) * B;
+    if (COLS) {
+        const int col = cg * 32 + lane;
+        const T s = row_sum_cols<T, false>(idx, a, b, F, B, col);
+        dst[col] = s + __ldg(F + (size_t)my * B + col);
+    } else {
+        for (int c = 0; c < B; c++) {
+            const T s = row_sum_lanes<T, false>(idx, a, b, F, B, c);
+            if (lane == 0) dst[c] = s + __ldg(F + (size_t)my * B + c);
+        }
+    }
+}
+
+cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *F,
+                              void *g, int64_t lo, int64_t hi, int64_t B, int out_rank,
+                              cudaStream_t s) {
+    if (hi <= lo) return cudaSuccess;
+    const bool cols = B % 32 == 0;
+    const int G = cols ? (int)(B / 32) : 1;
+    const int64_t warps = (hi - lo) * G;
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    launches_add(1);
+#define GCSR(TT, CC)                                                                             \
+    k_gather_csr<TT, CC><<<blocks, 256, 0, s>>>(P, C.ptr, C.idx, (const TT *)F, (TT *)g, lo, hi, \
+                                                (int32_t)B, G, out_rank)
+    if (dtype == 0) {
+        if (cols) GCSR(u64, true); else GCSR(u64, false);
+    } else {
+        if (cols) GCSR(double, true); else GCSR(double, false);
+    }
+#undef GCSR
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------ Möbius (CSR) ------
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T, bool COLS>
+__global__ void __launch_bounds__(512) k_moeb_csr(DevPoset P, const int64_t *__restrict__ ptr,
+                                                  const int32_t *__restrict__ idx,
+                                                  const T *__restrict__ g, T *F, T *__restrict__ f,
+                                                  int32_t B, int G, unsigned *bar) {
+    const int64_t TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int32_t L = 0; L < P.ell; L++) {
+        const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        const int64_t items = (int64_t)(hi - lo) * G;
+        for (int64_t it = gw; it < items; it += TW) {
+            const int32_t r = lo + (int32_t)(it / G);
+            const int cg = (int)(it % G);
+            const int64_t a = ptr[r], b = ptr[r + 1];
+            const int32_t my = P.slot[r], u = P.rank_user[r];
+            const bool has_prev = !(P.slot_user[my] < 0);   // bit 31 = chain start
+            if (COLS) {
+                const int col = cg * 32 + lane;
+                const T s = row_sum_cols<T, true>(idx, a, b, F, B, col);
+                const T Fx = __ldg(g + (size_t)u * B + col) - s;
+                F[(size_t)my * B + col] = Fx;
+                f[(size_t)u * B + col] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + col) : Fx;
+            } else {
+                for (int c = 0; c < B; c++) {
+                    const T s = row_sum_lanes<T, true>(idx, a, b, F, B, c);
+                    if (lane == 0) {
+                        const T Fx = __ldg(g + (size_t)u * B + c) - s;
+                        F[(size_t)my * B + c] = Fx;
+                        f[(size_t)u * B + c] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + c) : Fx;
+                    }
+                }
+            }
+        }
+        if (L + 1 < P.ell) grid_sync(bar, gridDim.x);
+    }
+}
+
+cudaError_t launch_moebius_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *g,
+                               void *F, void *f, int64_t B, unsigned *bar, int num_sms,
+                               cudaStream_t s) {
+    if (P.n == 0) return cudaSuccess;
+    const bool cols = B % 32 == 0;
+    int G = cols ? (int)(B / 32) : 1;
+    void *fn;
+    if (dtype == 0)
+        fn = cols ? (void *)k_moeb_csr<u64, true> : (void *)k_moeb_csr<u64, false>;
+    else
+        fn = cols ? (void *)k_moeb_csr<double, true> : (void *)k_moeb_csr<double, false>;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, 0);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(1, std::min(per_sm, 2));
+    e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    DevPoset Pc = P;
+    const int64_t *pp = C.ptr;
+    const int32_t *ip = C.idx;
+    int32_t Bi = (int32_t)B;
+    void *args[] = {&Pc, &pp, &ip, (void *)&g, &F, &f, &Bi, &G, &bar};
+    launches_add(1);
+    return cudaLaunchCooperativeKernel(fn, dim3(num_sms * per_sm), dim3(512), args, 0, s);
+}
+
+}  // namespace poset

@@ -13,14 +13,14 @@
 // and RING >= R + max level width, so a ring entry is never overwritten
 // while it can still be read.  Nothing but the result leaves the SM:
 //
-//   D   [npad][kp] uint16, rank-major ring-slot table: D[r][0] = ring slot
-//       of next(r), D[r][1+j] = ring slot of niv_j(r) for j ≠ id(r); ring
-//       slot of rank p = p mod RING; RING (the zero entry) where there is no
-//       dependency.  Built once per poset (k_build_dist).
+//   D   [npad][kp] uint16, rank-major ring-slot rows: the ring slots
+//       (rank mod RING) of niv_j(r) for j ≠ id(r), sorted by bank key,
+//       padded with RING (the zero entry); 64 entries per lane, LPE lanes
+//       per element.  Pn [npad]: ring slot of next(r) (RING at a chain
+//       bottom).  Built once per poset (k_build_dist).
 //
-// Per element the kernel sums S = Σ_row F[slot] over the whole row (the
-// predecessor included), so f(x) = g(x) - S directly and F(x) = f(x) +
-// F(next(x)) goes into the ring.  LPE lanes share one element's row.
+// Per element: F(x) = g(x) - Σ_row F[slot] goes into the ring and
+// f(x) = F(x) - F(next(x)) to global memory.
 //   gP  [B][npad] the input g permuted to rank order (k_to_rank_major).
 //
 // D, gP and rank->user rows are streamed into a NSTAGE-deep shared-memory
@@ -39,6 +39,13 @@
 namespace poset {
 
 typedef unsigned long long u64;
+
+template <typename T>
+__device__ __forceinline__ T from_bits(u64 x);
+template <>
+__device__ __forceinline__ u64 from_bits<u64>(u64 x) { return x; }
+template <>
+__device__ __forceinline__ double from_bits<double>(u64 x) { return __longlong_as_double((long long)x); }
 
 // ------------------------------------------------ setup: reach + table ----
 // max over (r, j) of r - rank(dep), dep = niv_j(r) (j ≠ id(r)) or next(r)
@@ -65,43 +72,74 @@ __global__ void k_reach_max(const int32_t *__restrict__ M, int32_t n, int32_t k,
     if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
-// D[r][*] (see header).  CTA = 32 ranks; the chain-major table is read in
-// coalesced 32-rank rows, transposed through shared memory, written as
-// contiguous rank rows.
+// D rows and next slots (see header).  CTA = 32 ranks: the chain-major
+// table is read in coalesced 32-rank rows into shared memory, each row is
+// counting-sorted by its bank key, and the rows are written out contiguous.
+// Bank key of a dependency slot s of rank r: ((s - r) mod 16) -- the ring
+// holds 8-byte entries, so slot s lives in bank pair s mod 16; after the sort,
+// the lanes of a warp (consecutive ranks) reading their q-th entries hit
+// different bank pairs instead of colliding at random.
 __global__ void __launch_bounds__(256) k_build_dist(const int32_t *__restrict__ M, int32_t n,
                                                     int32_t k, int32_t kp, int32_t ring,
                                                     const int32_t *__restrict__ chain,
                                                     const int32_t *__restrict__ slot,
                                                     const int32_t *__restrict__ slot_rank,
-                                                    uint16_t *__restrict__ D) {
-    extern __shared__ uint16_t tile[];   // [32][kp + 2]
+                                                    uint16_t *__restrict__ D, uint16_t *__restrict__ Pn) {
+    extern __shared__ uint16_t tile[];   // [2][32][kp + 2]
     const int stride = kp + 2;
+    uint16_t *raw = tile, *srt = tile + 32 * stride;
     const int r0 = blockIdx.x * 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int r = r0 + lane;
     const int mask = ring - 1;
-    for (int j = w; j < kp; j += nw) {
+    for (int j = w; j < k; j += nw) {
         int dep = -1;
         if (r < n) {
-            if (j == 0) {
-                const int32_t s = slot[r];
-                if (s > 0) {
-                    const int32_t p = slot_rank[s - 1];
-                    if (chain[p] == chain[r]) dep = p;
-                }
-            } else if (j <= k) {
-                const int32_t s = M[(size_t)(j - 1) * n + r];
-                if (s != n && chain[r] != j - 1) dep = slot_rank[s];
+            const int32_t s = M[(size_t)j * n + r];
+            if (s != n && chain[r] != j) dep = slot_rank[s];
+        }
+        raw[lane * stride + j] = (uint16_t)(dep >= 0 ? (dep & mask) : ring);
+    }
+    if (w == 0) {
+        int dep = -1;
+        if (r < n) {
+            const int32_t s = slot[r];
+            if (s > 0) {
+                const int32_t p = slot_rank[s - 1];
+                if (chain[p] == chain[r]) dep = p;
             }
         }
-        tile[lane * stride + j] = (uint16_t)(dep >= 0 ? (dep & mask) : ring);
+        Pn[r] = (uint16_t)(dep >= 0 ? (dep & mask) : ring);
+    }
+    __syncthreads();
+    if (w == 0) {   // counting sort of row `lane` by bank key; "none" entries last
+        int cnt[17];
+#pragma unroll
+        for (int c = 0; c < 17; c++) cnt[c] = 0;
+        const uint16_t *in = raw + lane * stride;
+        for (int j = 0; j < k; j++) {
+            const int s = in[j];
+            cnt[s == ring ? 16 : ((s - r) & 15)]++;
+        }
+        int pos[17], acc = 0;
+#pragma unroll
+        for (int c = 0; c < 17; c++) { pos[c] = acc; acc += cnt[c]; }
+        uint16_t *out = srt + lane * stride;
+        for (int j = 0; j < k; j++) {
+            const int s = in[j];
+            const int c = s == ring ? 16 : ((s - r) & 15);
+#pragma unroll
+            for (int cc = 0; cc < 17; cc++)
+                if (cc == c) out[pos[cc]++] = (uint16_t)s;
+        }
+        for (int j = k; j < kp; j++) out[j] = (uint16_t)ring;
     }
     __syncthreads();
     // rows r0..r0+31 are contiguous in D: write 16-bit words coalesced
     const int64_t base = (int64_t)r0 * kp;
     for (int t = threadIdx.x; t < 32 * kp; t += blockDim.x) {
         const int rr = t / kp, j = t % kp;
-        D[base + t] = tile[rr * stride + j];
+        D[base + t] = srt[rr * stride + j];
     }
 }
 
@@ -117,15 +155,14 @@ cudaError_t launch_reach_max(const DevPoset &P, const int32_t *slot_rank, unsign
 }
 
 cudaError_t launch_build_dist(const DevPoset &P, const int32_t *slot_rank, int32_t kp, int32_t ring,
-                              int64_t npad, uint16_t *D, cudaStream_t s) {
-    // padding rows/columns point at the zero entry (RING)
-    cudaError_t e = cudaMemsetAsync(D, 0, (size_t)npad * kp * 2, s);
-    if (e != cudaSuccess || P.n == 0) return e;
-    const size_t smem = (size_t)32 * (kp + 2) * 2;
+                              int64_t npad, uint16_t *D, uint16_t *Pn, cudaStream_t s) {
+    if (P.n == 0) return cudaSuccess;
+    const size_t smem = (size_t)2 * 32 * (kp + 2) * 2;
+    cudaError_t e;
     e = cudaFuncSetAttribute(k_build_dist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_build_dist<<<(unsigned)(npad / 32), 256, smem, s>>>(P.M, P.n, P.k, kp, ring, P.chain, P.slot,
-                                                          slot_rank, D);
+                                                          slot_rank, D, Pn);
     launches_add(1);
     return cudaGetLastError();
 }
@@ -197,7 +234,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 
 // ------------------------------------------------------- the kernel -------
 struct RingArgs {
-    const uint16_t *D;          // [npad][kp] ring-slot rows
+    const uint16_t *D;          // [npad][kp] sorted ring-slot rows
+    const uint16_t *Pn;         // [npad] ring slot of next(r)
     const void *gP;             // [B][npad]
     const int32_t *ru;          // [npad] rank -> user (padded)
     const int32_t *lvl_ptr;     // [ell + 1]
@@ -208,7 +246,62 @@ struct RingArgs {
     int32_t lg_ch, nstage;      // log2 ranks per staged chunk, pipeline depth (power of two)
 };
 
-template <typename T, int LPE>
+// 8 shared-memory loads in one asm block: issued back to back, so all 32
+// loads of a row chunk are in flight before the first add (the compiler's own
+// schedule interleaves them 4 at a time with the additions).
+__device__ __forceinline__ void lds64x8(unsigned base, const unsigned (&w)[4], u64 (&v)[8]) {
+    asm volatile(
+        "{\n\t.reg .u32 a<8>;\n\t"
+        "and.b32 a0, %8, 65535;\n\tshr.u32 a1, %8, 16;\n\t"
+        "and.b32 a2, %9, 65535;\n\tshr.u32 a3, %9, 16;\n\t"
+        "and.b32 a4, %10, 65535;\n\tshr.u32 a5, %10, 16;\n\t"
+        "and.b32 a6, %11, 65535;\n\tshr.u32 a7, %11, 16;\n\t"
+        "mad.lo.u32 a0, a0, 8, %12;\n\tmad.lo.u32 a1, a1, 8, %12;\n\t"
+        "mad.lo.u32 a2, a2, 8, %12;\n\tmad.lo.u32 a3, a3, 8, %12;\n\t"
+        "mad.lo.u32 a4, a4, 8, %12;\n\tmad.lo.u32 a5, a5, 8, %12;\n\t"
+        "mad.lo.u32 a6, a6, 8, %12;\n\tmad.lo.u32 a7, a7, 8, %12;\n\t"
+        "ld.shared.b64 %0, [a0];\n\tld.shared.b64 %1, [a1];\n\t"
+        "ld.shared.b64 %2, [a2];\n\tld.shared.b64 %3, [a3];\n\t"
+        "ld.shared.b64 %4, [a4];\n\tld.shared.b64 %5, [a5];\n\t"
+        "ld.shared.b64 %6, [a6];\n\tld.shared.b64 %7, [a7];\n\t}"
+        : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]), "=l"(v[4]), "=l"(v[5]), "=l"(v[6]),
+          "=l"(v[7])
+        : "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(base));
+}
+
+// Σ of the ring entries named by E consecutive row words (E/8 x LDS.128 of
+// slots, E independent LDS.64, balanced tree).
+template <typename T, int E>
+__device__ __forceinline__ T ring_sum(const T *ring, const uint16_t *row) {
+    T v[E];
+    if constexpr (E >= 8) {
+        uint4 w[E / 8];
+#pragma unroll
+        for (int i = 0; i < E / 8; i++) w[i] = reinterpret_cast<const uint4 *>(row)[i];
+#pragma unroll
+        for (int i = 0; i < E / 8; i++) {
+            const unsigned ws[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                v[8 * i + 2 * h] = ring[ws[h] & 0xffffu];
+                v[8 * i + 2 * h + 1] = ring[ws[h] >> 16];
+            }
+        }
+    } else {
+        const uint2 w = *reinterpret_cast<const uint2 *>(row);
+        v[0] = ring[w.x & 0xffffu];
+        v[1] = ring[w.x >> 16];
+        v[2] = ring[w.y & 0xffffu];
+        v[3] = ring[w.y >> 16];
+    }
+#pragma unroll
+    for (int st = 1; st < E; st <<= 1)
+#pragma unroll
+        for (int i = 0; i < E; i += 2 * st) v[i] += v[i + st];
+    return v[0];
+}
+
+template <typename T, int LPE, int E>
 __global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
@@ -216,13 +309,13 @@ __global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
     T *ring = reinterpret_cast<T *>(smem);                               // RING + 1 entries
     u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);  // nstage
     unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 1) & ~1);
-    const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
-    const unsigned sbytes = dbytes + gbytes + ubytes;
+    const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8;
+    const unsigned ubytes = (unsigned)ch * 4, pbytes = (unsigned)ch * 2;
+    const unsigned sbytes = dbytes + gbytes + ubytes + pbytes;
     const int b = blockIdx.x;
     const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
     const int sub = tid & (LPE - 1), grp = tid / LPE, NG = NT / LPE;
     const unsigned gmask = LPE == 32 ? 0xffffffffu : (((1u << LPE) - 1u) << (lane & ~(LPE - 1)));
-    const int Q = a.kp / LPE;   // row entries per lane (even)
     const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
     T *f = reinterpret_cast<T *>(a.f);
     const int32_t nchunks = (int32_t)(a.npad >> a.lg_ch);
@@ -237,10 +330,12 @@ __global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
     auto issue = [&](int32_t c) {
         const int s = c & (a.nstage - 1);
         unsigned char *st = stage0 + (size_t)s * sbytes;
+        const size_t r0 = (size_t)c << a.lg_ch;
         mbar_expect_tx(&bars[s], sbytes);
-        bulk_g2s(st, a.D + ((size_t)c << a.lg_ch) * a.kp, dbytes, &bars[s]);
-        bulk_g2s(st + dbytes, gcol + ((size_t)c << a.lg_ch), gbytes, &bars[s]);
-        bulk_g2s(st + dbytes + gbytes, a.ru + ((size_t)c << a.lg_ch), ubytes, &bars[s]);
+        bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s]);
+        bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s]);
+        bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
+        bulk_g2s(st + dbytes + gbytes + ubytes, a.Pn + r0, pbytes, &bars[s]);
     };
     if (tid == 0)
         for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
@@ -263,30 +358,16 @@ __global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
         for (int32_t e = lo + grp; e < hi; e += NG) {   // uniform within an LPE group
             const int off = e & (ch - 1);
             const unsigned char *st = stage0 + (size_t)((e >> a.lg_ch) & (a.nstage - 1)) * sbytes;
-            const uint16_t *row = reinterpret_cast<const uint16_t *>(st) + (size_t)off * a.kp + sub * Q;
-            const unsigned dpred = row[0];   // meaningful in sub 0 (entry 0 of the row)
-            T s = T(0);
-            for (int q = 0; q < Q; q += 8) {
-                unsigned w[4];
-#pragma unroll
-                for (int h = 0; h < 4; h++)
-                    w[h] = (q + 2 * h < Q) ? *reinterpret_cast<const unsigned *>(row + q + 2 * h)
-                                           : (unsigned)RING * 0x10001u;
-                T v[8];
-#pragma unroll
-                for (int h = 0; h < 4; h++) {
-                    v[2 * h] = ring[w[h] & 0xffffu];
-                    v[2 * h + 1] = ring[w[h] >> 16];
-                }
-                s += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-            }
+            const uint16_t *row = reinterpret_cast<const uint16_t *>(st) + (size_t)off * a.kp + sub * E;
+            T s = ring_sum<T, E>(ring, row);
 #pragma unroll
             for (int o = LPE / 2; o; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
             if (sub == 0) {
-                const T fx = reinterpret_cast<const T *>(st + dbytes)[off] - s;
+                const T Fx = reinterpret_cast<const T *>(st + dbytes)[off] - s;
                 const int32_t u = reinterpret_cast<const int32_t *>(st + dbytes + gbytes)[off];
-                f[(size_t)u * a.B + b] = fx;
-                ring[e & a.ring_mask] = fx + ring[dpred];
+                const unsigned pn = reinterpret_cast<const uint16_t *>(st + dbytes + gbytes + ubytes)[off];
+                f[(size_t)u * a.B + b] = Fx - ring[pn];
+                ring[e & a.ring_mask] = Fx;
             }
         }
         if (NT == 32) __syncwarp();
@@ -307,20 +388,18 @@ void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsig
                RingPlan &R) {
     R.ok = false;
     R.reach = reach;
-    if (n <= 0 || k + 1 > 2048) return;
+    if (n <= 0 || k > 256) return;
     int64_t ring = 32;
     while (ring < (int64_t)reach + max_level_width + 1) ring <<= 1;
     if (ring > (1 << 15)) return;   // ring slots are uint16, RING itself included
+    const int entries = k <= 64 ? 64 : k <= 128 ? 128 : 256;
+    // row stride = 16 B x odd: consecutive rows start in different bank quads
+    const int32_t kp = entries + 8;
+    const int lpe = std::min(32, entries / 8);   // 8 entries per lane (measured best)
     const double avg_w = (double)n / std::max(ell, 1);
-    int lpe = 4;
-    while (lpe > 1 && avg_w * lpe > 512) lpe >>= 1;
-    // row = [pred, chain 0 .. k-1], padded to 8*lpe entries
-    const int32_t unit = 8 * lpe;
-    const int32_t kp = (k + 1 + unit - 1) / unit * unit;
-    int threads = (int)std::min<int64_t>(512, ((int64_t)std::ceil(avg_w * lpe) + 31) / 32 * 32);
-    threads = std::max(threads, 32);
+    (void)avg_w;
     for (int nstage : {4, 2}) {
-        for (int ch : {256, 128, 64, 32, 16, 8, 4}) {
+        for (int ch : {256, 128, 64, 32, 16, 8}) {
             if ((int64_t)max_level_width > (int64_t)(nstage - 1) * ch) break;
             if (ring_smem_bytes((int)ring, kp, ch, nstage) <= kSmemCap) {
                 R.ok = true;
@@ -329,7 +408,7 @@ void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsig
                 R.ch = ch;
                 R.nstage = nstage;
                 R.lpe = lpe;
-                R.threads = threads;
+                R.entries = entries;
                 R.npad = ((int64_t)n + ch - 1) / ch * ch;
                 return;
             }
@@ -339,7 +418,7 @@ void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsig
 
 size_t ring_smem_bytes(int ring, int kp, int ch, int nstage) {
     return (size_t)(ring + 2) * 8 + 8 * ((nstage + 1) & ~1) +
-           (size_t)nstage * ch * ((size_t)kp * 2 + 8 + 4);
+           (size_t)nstage * ch * ((size_t)kp * 2 + 8 + 4 + 2);
 }
 
 cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype, const void *gP,
@@ -347,6 +426,7 @@ cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype,
     if (P.n == 0) return cudaSuccess;
     RingArgs a;
     a.D = R.D;
+    a.Pn = R.Pn;
     a.gP = gP;
     a.ru = R.ru_pad;
     a.lvl_ptr = P.lvl_ptr;
@@ -361,15 +441,24 @@ cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype,
     while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
     a.nstage = R.nstage;
     const size_t smem = ring_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
-    void *fn;
-#define RING_FN(LPE) (dtype == 0 ? (void *)k_moeb_ring<u64, LPE> : (void *)k_moeb_ring<double, LPE>)
-    fn = R.lpe == 4 ? RING_FN(4) : R.lpe == 2 ? RING_FN(2) : RING_FN(1);
+    const int lpe = R.lpe, E = R.entries / R.lpe;
+    void *fn = nullptr;
+#define RING_FN(L, EE)                                                                          \
+    if (lpe == L && E == EE)                                                                    \
+        fn = dtype == 0 ? (void *)k_moeb_ring<u64, L, EE> : (void *)k_moeb_ring<double, L, EE>;
+    RING_FN(1, 64) RING_FN(2, 32) RING_FN(4, 16) RING_FN(8, 8) RING_FN(16, 4)
+    RING_FN(2, 64) RING_FN(4, 32) RING_FN(8, 16) RING_FN(16, 8) RING_FN(32, 4)
+    RING_FN(4, 64) RING_FN(8, 32) RING_FN(16, 16) RING_FN(32, 8)
 #undef RING_FN
+    if (!fn) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    const double avg_w = (double)P.n / std::max(P.ell, 1);
+    int threads = (int)std::min<int64_t>(512, ((int64_t)std::ceil(avg_w * lpe) + 31) / 32 * 32);
+    threads = std::max(threads, 32);
     void *args[] = {&a};
     launches_add(1);
-    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(R.threads), args, smem, s);
+    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(threads), args, smem, s);
 }
 
 }  // namespace poset

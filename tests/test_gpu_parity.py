@@ -21,13 +21,15 @@ import paper_2211_13706_b200 as pz  # noqa: E402
 from oracle import brute  # noqa: E402
 from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
 
-KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING]
+KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING, pz.MOEB_CSR]
 
 
 def kernels_for(P):
-    """Every Möbius schedule that applies to P (RING needs a bounded reach)."""
-    ring_ok = P.info()["dist_bytes"] > 0
-    return [k for k in KERNELS if k != pz.MOEB_RING or ring_ok]
+    """Every Möbius schedule that applies to P (RING needs a bounded reach,
+    CSR needs the sparse rows, built when RING does not apply)."""
+    info = P.info()
+    return [k for k in KERNELS
+            if (k != pz.MOEB_RING or info["dist_bytes"] > 0) and (k != pz.MOEB_CSR or info["csr_bytes"] > 0)]
 facts = load_facts()
 PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
 
@@ -218,9 +220,12 @@ def test_ring_schedule_selection_and_limits():
         assert (gpu_moebius(P, g) == f).all(), B
         h = W.int_values(n, B, -10**17, 10**17, seed=B + 9)
         assert (gpu_moebius(P, h, pz.MOEB_RING) == O.moebius(h)).all(), B
-    # wide levels (Boolean lattice 2^12: 924-element middle level) do not fit
+    # wide levels (Boolean lattice 2^12: 924-element middle level) do not fit;
+    # there AUTO takes the sparse-row schedule
     Pb = pz.Poset(4096, *W.boolean_lattice(12))
     assert Pb.info()["dist_bytes"] == 0
+    assert Pb.info()["csr_bytes"] > 0 and Pb.info()["moebius_kernel"] == pz.MOEB_CSR
+    assert Pb.info()["zeta_sparse"] == 1            # fill < 1/2: zeta over the sparse rows
     Pb.set_option("moebius_kernel", pz.MOEB_RING)
     with pytest.raises(pz.PosetError) as e:
         Pb.moebius(dev(np.zeros((4096, 1), np.int64)))
