@@ -38,7 +38,7 @@ PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
                 "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
                 "chain_diff": "k_chain_diff"}
-MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr"]
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws"]
 
 
 def parse():
@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="functions per rank")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--moebius-kernel", default="auto", choices=MOEB_NAMES)
+    ap.add_argument("--gather-variant", type=int, default=0, help="dense gather kernel for B%%32==0 (tuning)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -136,7 +137,13 @@ def alg_bytes(n, k, B, info=None):
         "moebius_solve": 4 * n * k + 24 * n * B + 8 * n,   # index, g read, F write + read once
         "chain_diff": 16 * n * B + 4 * n,
     }
-    if info is not None and info.get("moebius_kernel") == 4:
+    if info is not None and info.get("zeta_sparse"):
+        # sparse U-rows: 4 bytes per stored entry + row pointers instead of 4nk
+        sparse = info["csr_bytes"] + 8 * n
+        d["gather"] = sparse + 16 * n * B + 4 * n
+    if info is not None and info.get("moebius_kernel") == 5:
+        d["moebius_solve"] = info["csr_bytes"] + 32 * n * B + 8 * n   # rows, g, F w+r, f
+    if info is not None and info.get("moebius_kernel") in (4, 6):
         # RING: distance table once (shared by the B CTAs through L2), gP read,
         # f written, rank->user rows; F never leaves shared memory
         d["moebius_solve"] = info["dist_bytes"] + 16 * n * B + 4 * n
@@ -214,6 +221,7 @@ def main():
     info = P.info()
     kern = MOEB_NAMES.index(args.moebius_kernel)
     P.set_option("moebius_kernel", kern)
+    P.set_option("gather_variant", args.gather_variant)
     f_host = wl.values(seed=1 + rank)
     x = torch.from_numpy(f_host).cuda()
     g = torch.empty_like(x)

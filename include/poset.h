@@ -73,8 +73,11 @@ typedef enum {
     POSET_MOEB_WARP = 3,      /* one warp per column group sweeps all levels (no grid sync) */
     POSET_MOEB_RING = 4,      /* bounded-reach posets: one CTA per column, F in a shared-memory
                                  ring, U-solve and chain difference fused   */
-    POSET_MOEB_CSR = 5        /* sparse U-rows, persistent kernel with a grid barrier per
+    POSET_MOEB_CSR = 5,       /* sparse U-rows, persistent kernel with a grid barrier per
                                  level, one warp per (element, column group) */
+    POSET_MOEB_RINGWS = 6     /* RING with warp specialisation: one warp on the level-by-level
+                                 critical path (near dependencies only), the others summing the
+                                 far dependencies ahead of it                 */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -100,6 +103,7 @@ typedef struct {
     double t_dist;        /* seconds: reach + distance table + sparse rows build    */
     int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
+    int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
 } poset_info;
 
 /*
@@ -190,6 +194,9 @@ poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64
 poset_status poset_query(poset_t h, poset_info *out);
 
 /* poset_set_option -- "moebius_kernel" (poset_moebius_kernel value);
+ * "ring_lpe" (lanes per element of the RING schedule, tuning);
+ * "gather_variant" (process-wide dense zeta gather for batch % 32 == 0:
+ * 0 = per-lane row reuse (default), 1 = lanes over columns, 2 = lanes over ranks);
  * "profile" (0/1): record a CUDA event pair on the call's stream around every
  * kernel phase of subsequent calls (see poset_profile_read). */
 poset_status poset_set_option(poset_t h, const char *key, int64_t value);

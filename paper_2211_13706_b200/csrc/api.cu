@@ -37,6 +37,7 @@ struct poset_s {
     unsigned *d_bar = nullptr;
     unsigned long long *d_count = nullptr;
     RingPlan ring;                    // RING Möbius schedule (moebius_ring.cu)
+    RingWSPlan rws;                   // RINGWS Möbius schedule (moebius_ringws.cu)
     CsrRows csr;                      // sparse U-rows (moebius_csr.cu)
     bool zeta_csr = false;            // zeta gathers over the CSR rows (sparse table)
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
@@ -90,7 +91,7 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->d_gP, h->csr.ptr, h->csr.idx};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->d_gP, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -143,42 +144,52 @@ static poset_status finish_setup(poset_s *h) {
     CK(cudaMemcpy(&nnz, h->d_count, sizeof nnz, cudaMemcpyDeviceToHost));
     CK(cudaDeviceSynchronize());
     double t2 = now_seconds();
-    // RING schedule data: reach of the dependencies, then the rank-major
-    // distance table D if the plan fits shared memory and device memory.
+    // RING / RINGWS schedule data: reach of the dependencies, the plans, then
+    // the rank-major ring-slot tables if they fit shared and device memory.
     {
-        int32_t *d_slot_rank = nullptr;
+        int32_t *d_slot_rank = nullptr, *d_level = nullptr;
         CK(upload(&d_slot_rank, H.slot_rank));
-        unsigned reach = 0;
+        CK(upload(&d_level, H.level));
+        unsigned reach = 0, near3[3] = {0, 0, 0};
         cudaError_t e = launch_reach_max(P, d_slot_rank, (unsigned *)h->d_count, 0);
         if (e == cudaSuccess) e = cudaMemcpy(&reach, h->d_count, sizeof reach, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) { cudaFree(d_slot_rank); CK(e); }
+        if (e == cudaSuccess) e = launch_near_max(P, d_level, d_slot_rank, (unsigned *)h->d_count, 0);
+        if (e == cudaSuccess) e = cudaMemcpy(near3, h->d_count, sizeof near3, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { cudaFree(d_slot_rank); cudaFree(d_level); CK(e); }
         ring_plan(H.n, H.k, H.ell, H.max_level_width, reach, h->ring);
-        if (h->ring.ok) {
-            size_t dbytes = (size_t)h->ring.npad * h->ring.kp * 2;
-            size_t fb = 0, tb = 0;
-            cudaMemGetInfo(&fb, &tb);
-            if (dbytes + (size_t)h->ring.npad * 6 + ((size_t)1 << 30) > fb ||
-                cudaMalloc((void **)&h->ring.D, dbytes) != cudaSuccess ||
-                cudaMalloc((void **)&h->ring.Pn, (size_t)h->ring.npad * 2) != cudaSuccess ||
-                cudaMalloc((void **)&h->ring.ru_pad, (size_t)h->ring.npad * 4) != cudaSuccess) {
-                cudaGetLastError();
-                if (h->ring.D) cudaFree(h->ring.D);
-                if (h->ring.Pn) cudaFree(h->ring.Pn);
-                h->ring.D = nullptr;
-                h->ring.Pn = nullptr;
-                h->ring.ok = false;
-            }
+        ringws_plan(H.n, H.k, H.max_level_width, reach, near3, h->rws);
+        const int64_t npad = ((int64_t)H.n + 255) / 256 * 256;   // common to both plans
+        h->ring.npad = npad;
+        h->rws.npad = npad;
+        size_t fb = 0, tb = 0;
+        cudaMemGetInfo(&fb, &tb);
+        const size_t reserve = (size_t)1 << 30;
+        auto alloc = [&](void **p, size_t bytes) {
+            if (bytes + reserve > fb || cudaMalloc(p, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+            fb -= bytes;
+            return true;
+        };
+        if ((h->ring.ok || h->rws.ok) && !alloc((void **)&h->ring.ru_pad, (size_t)npad * 4)) {
+            h->ring.ok = false;
+            h->rws.ok = false;
         }
-        if (h->ring.ok) {
-            e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, h->ring.npad, h->ring.D,
-                                  h->ring.Pn, 0);
-            if (e == cudaSuccess) e = cudaMemset(h->ring.ru_pad, 0, (size_t)h->ring.npad * 4);
+        if (h->ring.ok && !(alloc((void **)&h->ring.D, (size_t)npad * h->ring.kp * 2) &&
+                            alloc((void **)&h->ring.Pn, (size_t)npad * 2)))
+            h->ring.ok = false;
+        if (h->rws.ok && !alloc((void **)&h->rws.D, (size_t)npad * h->rws.kp * 2)) h->rws.ok = false;
+        e = cudaSuccess;
+        if (h->ring.ok || h->rws.ok) {
+            e = cudaMemset(h->ring.ru_pad, 0, (size_t)npad * 4);
             if (e == cudaSuccess)
                 e = cudaMemcpy(h->ring.ru_pad, h->d_rank_user, (size_t)H.n * 4, cudaMemcpyDeviceToDevice);
-            if (e == cudaSuccess) e = cudaDeviceSynchronize();
-            if (e != cudaSuccess) { cudaFree(d_slot_rank); CK(e); }
         }
-        CK(cudaFree(d_slot_rank));
+        if (e == cudaSuccess && h->ring.ok)
+            e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, npad, h->ring.D, h->ring.Pn, 0);
+        if (e == cudaSuccess && h->rws.ok) e = launch_build_ringws(P, h->rws, d_level, d_slot_rank, 0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaFree(d_slot_rank);
+        cudaFree(d_level);
+        CK(e);
     }
     // sparse U-rows: for the Möbius solve when RING does not apply, and for
     // the zeta gather when the dense table is mostly ∞ (fill < 1/2)
@@ -209,11 +220,14 @@ static poset_status finish_setup(poset_s *h) {
     I.t_mtable = t2 - t1;
     I.device = h->device;
     I.reach = h->ring.reach;
-    I.dist_bytes = h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0;
+    I.dist_bytes = (h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0) +
+                   (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0);
+    I.ringws = h->rws.ok ? 1 : 0;
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
-    I.moebius_kernel = h->ring.ok  ? MOEB_RING
+    I.moebius_kernel = h->rws.ok   ? MOEB_RINGWS
+                       : h->ring.ok  ? MOEB_RING
                        : h->csr.ok ? MOEB_CSR
                                    : moebius_pick(P, 1, H.max_level_width, h->num_sms);
     // drop host arrays only the device needs
@@ -375,6 +389,7 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
     if (st) return st;
     DevPoset P = h->dev();
     int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
+                : h->rws.ok  ? MOEB_RINGWS
                 : h->ring.ok ? MOEB_RING
                 : h->csr.ok  ? MOEB_CSR
                              : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
@@ -387,6 +402,19 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
+    if (which == MOEB_RINGWS) {
+        if (!h->rws.ok)
+            return fail(POSET_EINVAL, "poset_moebius: the RINGWS schedule does not fit this poset; use AUTO");
+        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rws.npad * 8);
+        if (st) return st;
+        {
+            PhaseTimer t(h, POSET_PH_PERM, s);
+            CK(launch_to_rank_major(P, dt, g, B, h->rws.npad, h->d_gP, s));
+        }
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_ringws(P, h->rws, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+        return POSET_OK;
+    }
     if (which == MOEB_RING) {
         if (!h->ring.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RING schedule does not fit this poset "
@@ -573,7 +601,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_CSR) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RINGWS) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }
@@ -584,6 +612,28 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
             return fail(POSET_EINVAL, "poset_set_option: ring_lpe must be a power of two with "
                                       "4 <= entries/ring_lpe <= 64");
         h->ring.lpe = (int32_t)value;
+        return POSET_OK;
+    }
+    if (!strcmp(key, "ringws_nwo") || !strcmp(key, "ringws_lpeo")) {   // RINGWS tuning
+        if (!h->rws.ok) return fail(POSET_EINVAL, "poset_set_option: RINGWS is not available");
+        if (!strcmp(key, "ringws_nwo")) {
+            if (value != 4 && value != 8 && value != 12) return fail(POSET_EINVAL, "ringws_nwo is 4, 8 or 12");
+            h->rws.nwo = (int32_t)value;
+        } else {
+            const int64_t E = h->rws.fe / (value > 0 ? value : 1);
+            if (value < 4 || value > 32 || (value & (value - 1)) || (E != 8 && E != 16))
+                return fail(POSET_EINVAL, "ringws_lpeo must leave 8 or 16 far entries per lane");
+            h->rws.lpeo = (int32_t)value;
+        }
+        return POSET_OK;
+    }
+    if (!strcmp(key, "ring_debug")) {   // timing experiments only: results are NOT valid
+        h->ring.debug = (int32_t)value;
+        return POSET_OK;
+    }
+    if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)
+        if (value < 0 || value > 2) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0, 1 or 2");
+        set_gather_variant((int)value);
         return POSET_OK;
     }
     if (!strcmp(key, "profile")) {

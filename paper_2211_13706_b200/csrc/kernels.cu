@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -575,6 +576,96 @@ __global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restric
     }
 }
 
+// Lanes over (rank, 4 columns) -- B % 32 == 0, the batched configs.  A warp
+// owns 16 consecutive ranks: lane group q = lane / 8 (4 groups) walks ranks
+// 4q .. 4q+3 one after the other, lane l % 8 owns columns 4(l%8) .. 4(l%8)+3
+// of a 32-column group.  For each chain j a lane keeps the F row it last
+// used (4 values) in registers and reloads it -- one predicated 32-byte load
+// straight into the held registers -- only when the chain's index changes
+// from the previous rank (the "run" structure of chain-local posets).  Per
+// (rank, chain, 32 columns) this costs 1/4 of a compare, address and load
+// issue plus the 32 adds, against ~7 instructions of the lanes-over-columns
+// form.  Index chunks (64 chains x 16 ranks per warp) are staged by cp.async.
+__device__ __forceinline__ void ld4_if_ne(u64 (&v)[4], const void *p, int32_t a, int32_t b) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %4, %5;\n\t"
+                 "@q ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%6];\n\t}"
+                 : "+l"(v[0]), "+l"(v[1]), "+l"(v[2]), "+l"(v[3])
+                 : "r"(a), "r"(b), "l"(p));
+}
+
+template <typename T, int KCH>
+__global__ void __launch_bounds__(256, 2) k_gather_r4(const int32_t *__restrict__ M, int32_t n,
+                                                      int32_t k, const T *__restrict__ F,
+                                                      T *__restrict__ out,
+                                                      const int32_t *__restrict__ rank_user,
+                                                      int64_t row_lo, int64_t row_hi, int32_t B,
+                                                      int G32, int mode) {
+    constexpr int TS = 4, KC = 4, TRW = 16;   // ranks per lane, chains per step, ranks per warp
+    __shared__ __align__(16) int32_t sid[8][TRW][KCH];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = lane >> 3, cq = lane & 7;
+    const int cg = (int)(blockIdx.x % G32);
+    const int64_t tile = blockIdx.x / G32;
+    const int64_t r0 = row_lo + (tile * 8 + warp) * TRW;
+    if (r0 >= row_hi) return;
+    const int col0 = cg * 32 + cq * 4;
+    const char *Fb = reinterpret_cast<const char *>(F + col0);
+    const unsigned rowbytes = (unsigned)B * sizeof(T);
+    int32_t (*S)[KCH] = sid[warp];
+    T acc[TS][4];
+#pragma unroll
+    for (int ts = 0; ts < TS; ts++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc[ts][c] = T(0);
+    for (int j0 = 0; j0 < k; j0 += KCH) {
+        __syncwarp();
+        // word w: chain w / TRW, rank w % TRW (16 consecutive ranks = 64 B)
+#pragma unroll 4
+        for (int i = 0; i < KCH * TRW / 32; i++) {
+            const int w = i * 32 + lane, jj = w / TRW, t = w % TRW;
+            const int64_t r = r0 + t;
+            if (j0 + jj < k && r < row_hi)
+                cp_async4(&S[t][jj], M + (size_t)(j0 + jj) * n + r);
+            else
+                S[t][jj] = n;   // the zero row of F
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        const int jn = min(KCH, k - j0);
+        for (int jj = 0; jj < jn; jj += KC) {
+            u64 v[KC][4];
+            int32_t prev[KC];
+#pragma unroll
+            for (int u = 0; u < KC; u++) prev[u] = -1;   // never an index: first rank loads
+#pragma unroll
+            for (int ts = 0; ts < TS; ts++) {
+                const int4 id4 = *reinterpret_cast<const int4 *>(&S[q * TS + ts][jj]);
+                const int32_t id[KC] = {id4.x, id4.y, id4.z, id4.w};
+#pragma unroll
+                for (int u = 0; u < KC; u++) {
+                    ld4_if_ne(v[u], Fb + (size_t)(unsigned)id[u] * rowbytes, id[u], prev[u]);
+                    prev[u] = id[u];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    acc[ts][c] += (from_bits<T>(v[0][c]) + from_bits<T>(v[1][c])) +
+                                  (from_bits<T>(v[2][c]) + from_bits<T>(v[3][c]));
+            }
+        }
+    }
+#pragma unroll
+    for (int ts = 0; ts < TS; ts++) {
+        const int64_t r = r0 + q * TS + ts;
+        if (r < row_hi) {
+            T *dst = mode == 0 ? out + (size_t)rank_user[r] * B : out + (size_t)(r - row_lo) * B;
+            u64 o[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) o[c] = to_bits<T>(acc[ts][c]);
+            stv<4>(reinterpret_cast<u64 *>(dst + col0), o);
+        }
+    }
+}
+
 template <typename T>
 __global__ void k_gather_reduce(const T *__restrict__ part, T *__restrict__ out,
                                 const int32_t *__restrict__ rank_user, int64_t row_lo,
@@ -590,6 +681,13 @@ __global__ void k_gather_reduce(const T *__restrict__ part, T *__restrict__ out,
     else
         out[(size_t)rr * B + b] = acc;
 }
+
+// Dense-gather variant for B % 32 == 0 (process-wide; poset_set_option
+// "gather_variant"): 0 = k_gather_r4 (default), 1 = k_gather_cols,
+// 2 = k_gather (lanes over ranks).
+static std::atomic<int> g_gather_variant{0};
+void set_gather_variant(int v) { g_gather_variant = v; }
+static int gather_variant() { return g_gather_variant.load(); }
 
 static int gather_cb(int64_t B) {
     for (int cb : {8, 4, 2, 1})
@@ -650,7 +748,15 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
                             int64_t B, int mode, void *partial, int num_sms, cudaStream_t s) {
     int S = gather_slices(P, hi - lo, B, num_sms);
     if (S > 1 && !partial) S = 1;
-    if (B % 32 == 0 && S == 1) {
+    if (B % 32 == 0 && S == 1 && gather_variant() == 0) {
+        const int G32 = (int)(B / 32);
+        const int64_t tiles = (hi - lo + 8 * 16 - 1) / (8 * 16);
+        k_gather_r4<T, 64><<<(unsigned)(tiles * G32), 256, 0, s>>>(
+            P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+        COUNT_LAUNCH(1);
+        return cudaGetLastError();
+    }
+    if (B % 32 == 0 && S == 1 && gather_variant() == 1) {
         constexpr int TR = 8, KCH = 64;
         const int G32 = (int)(B / 32);
         const int64_t tiles = (hi - lo + 8 * TR - 1) / (8 * TR);

@@ -47,13 +47,15 @@ cudaError_t launch_combine_tails(int dtype, const void *tails, int64_t world, in
 // rows [row_lo, row_hi).  out_rank != 0: write g_rank[r - row_lo] (rank order)
 // instead of g[user(r)].  partial: scratch for j-slicing (may be null if
 // gather_partial_bytes() == 0).
+void set_gather_variant(int v);   // 0 r4 (default), 1 cols, 2 lanes over ranks (B % 32 == 0)
 size_t gather_partial_bytes(const DevPoset &P, int64_t rows, int64_t batch, int num_sms);
 cudaError_t launch_gather(const DevPoset &P, int dtype, const void *F, void *g, int64_t row_lo,
                           int64_t row_hi, int64_t batch, int out_rank, void *partial,
                           int num_sms, cudaStream_t s);
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
-enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5 };
+enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5,
+                  MOEB_RINGWS = 6 };
 int moebius_pick(const DevPoset &P, int64_t batch, int max_level_width, int num_sms);
 cudaError_t launch_moebius_solve(const DevPoset &P, const int32_t *h_lvl_ptr, int dtype,
                                  const void *g, void *F, int64_t batch, int which,
@@ -78,6 +80,7 @@ struct RingPlan {
     int32_t ch = 0, nstage = 0; // ranks per staged chunk, pipeline depth
     int32_t entries = 0;        // row entries (64, 128 or 256 >= k)
     int32_t lpe = 1;            // lanes per element; entries / lpe per lane (8..64)
+    int32_t debug = 0;          // tuning experiments (poset_set_option "ring_debug")
     int64_t npad = 0;           // n rounded up to a multiple of ch
     uint16_t *D = nullptr;      // [npad][kp]
     uint16_t *Pn = nullptr;     // [npad] ring slot of next(r)
@@ -96,6 +99,30 @@ cudaError_t launch_to_rank_major(const DevPoset &P, int dtype, const void *g, in
                                  int64_t npad, void *gP, cudaStream_t s);
 cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype, const void *gP,
                                 void *f, int64_t B, cudaStream_t s);
+
+// ---- kernel (v), RINGWS schedule (moebius_ringws.cu): RING with a fresh
+// warp on the level-by-level critical path and old warps summing the far
+// dependencies ahead of it ----
+struct RingWSPlan {
+    bool ok = false;
+    int32_t ld = 0;             // near = dependencies at level distance <= ld
+    int32_t nn = 0, fe = 0;     // near / far row entries
+    int32_t kp = 0;             // row stride (uint16 words)
+    int32_t ring = 0, sbuf = 0; // ring entries, S_old buffer entries (powers of two)
+    int32_t ch = 0, nstage = 0;
+    int32_t lpeo = 0;           // old-warp lanes per element
+    int32_t nwo = 0;            // old warps per CTA (4, 8, 12)
+    int64_t npad = 0;
+    uint16_t *D = nullptr;      // [npad][kp]
+};
+void ringws_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
+                 const unsigned near_max[3], RingWSPlan &R);
+cudaError_t launch_near_max(const DevPoset &P, const int32_t *level, const int32_t *slot_rank,
+                            unsigned *out3, cudaStream_t s);
+cudaError_t launch_build_ringws(const DevPoset &P, const RingWSPlan &R, const int32_t *level,
+                                const int32_t *slot_rank, cudaStream_t s);
+cudaError_t launch_moebius_ringws(const DevPoset &P, const RingWSPlan &R, const int32_t *ru_pad,
+                                  int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
 
 // ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----
 struct CsrRows {

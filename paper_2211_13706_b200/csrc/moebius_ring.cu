@@ -35,17 +35,12 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace poset {
 
 typedef unsigned long long u64;
 
-template <typename T>
-__device__ __forceinline__ T from_bits(u64 x);
-template <>
-__device__ __forceinline__ u64 from_bits<u64>(u64 x) { return x; }
-template <>
-__device__ __forceinline__ double from_bits<double>(u64 x) { return __longlong_as_double((long long)x); }
 
 // ------------------------------------------------ setup: reach + table ----
 // max over (r, j) of r - rank(dep), dep = niv_j(r) (j ≠ id(r)) or next(r)
@@ -201,37 +196,6 @@ cudaError_t launch_to_rank_major(const DevPoset &P, int dtype, const void *g, in
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------ PTX helpers -------
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(u64 *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64 *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64 *bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, u64 *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 // ------------------------------------------------------- the kernel -------
 struct RingArgs {
     const uint16_t *D;          // [npad][kp] sorted ring-slot rows
@@ -244,6 +208,7 @@ struct RingArgs {
     int32_t n, kp, ell, B;
     int32_t ring_mask;          // RING - 1 (power of two)
     int32_t lg_ch, nstage;      // log2 ranks per staged chunk, pipeline depth (power of two)
+    int32_t debug;              // tuning experiments only: bit 0 = skip the global store of f
 };
 
 // 8 shared-memory loads in one asm block: issued back to back, so all 32
@@ -366,7 +331,7 @@ __global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
                 const T Fx = reinterpret_cast<const T *>(st + dbytes)[off] - s;
                 const int32_t u = reinterpret_cast<const int32_t *>(st + dbytes + gbytes)[off];
                 const unsigned pn = reinterpret_cast<const uint16_t *>(st + dbytes + gbytes + ubytes)[off];
-                f[(size_t)u * a.B + b] = Fx - ring[pn];
+                if (!(a.debug & 1)) f[(size_t)u * a.B + b] = Fx - ring[pn];
                 ring[e & a.ring_mask] = Fx;
             }
         }
@@ -440,6 +405,7 @@ cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype,
     a.lg_ch = 0;
     while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
     a.nstage = R.nstage;
+    a.debug = R.debug;
     const size_t smem = ring_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
     const int lpe = R.lpe, E = R.entries / R.lpe;
     void *fn = nullptr;

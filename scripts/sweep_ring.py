@@ -14,6 +14,7 @@ x = torch.from_numpy(wl.values(seed=1)).cuda()
 g = P.zeta(x)
 y = torch.empty_like(x)
 res = {"cfg": cfg, "n": wl.n, "k": info["k"], "ell": info["ell"], "reach": info["reach"]}
+P.set_option("moebius_kernel", pz.MOEB_RING)
 for lpe in (1, 2, 4, 8, 16):
     try:
         P.set_option("ring_lpe", lpe)
@@ -27,4 +28,58 @@ for lpe in (1, 2, 4, 8, 16):
     ms = prof["moebius_solve"][0] / 3
     res[f"lpe{lpe}_ms"] = ms
     res[f"lpe{lpe}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
+for kern, name in ((pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
+    if kern == pz.MOEB_RINGWS and not info["ringws"]:
+        continue
+    P.set_option("ring_lpe", 8)
+    P.set_option("moebius_kernel", kern)
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    P.set_option("profile", 1); P.profile_read()
+    for _ in range(3):
+        P.moebius(g, out=y)
+    prof, _ = P.profile_read(); P.set_option("profile", 0)
+    ms = prof["moebius_solve"][0] / 3
+    res[f"{name}_ms"] = ms
+    res[f"{name}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
+    if wl.dtype == "i64" or True:
+        xb = x if wl.dtype == "i64" else None
+if info["ringws"]:
+    P.set_option("moebius_kernel", pz.MOEB_RINGWS)
+    for nwo in (4, 8, 12):
+        for lpeo in (4, 8):
+            try:
+                P.set_option("ringws_nwo", nwo); P.set_option("ringws_lpeo", lpeo)
+            except pz.PosetError:
+                continue
+            P.moebius(g, out=y); torch.cuda.synchronize()
+            P.set_option("profile", 1); P.profile_read()
+            for _ in range(3):
+                P.moebius(g, out=y)
+            prof, _ = P.profile_read(); P.set_option("profile", 0)
+            ms = prof["moebius_solve"][0] / 3
+            res[f"ws_nwo{nwo}_lpeo{lpeo}_clk"] = ms * 1e-3 * 1.965e9 / info["ell"]
+    P.set_option("ringws_nwo", 8); P.set_option("ringws_lpeo", 8)
+# experiment: RING lpe 8 without the global store of f (output invalid)
+P.set_option("moebius_kernel", pz.MOEB_RING); P.set_option("ring_lpe", 8); P.set_option("ring_debug", 1)
+P.moebius(g, out=y); torch.cuda.synchronize()
+P.set_option("profile", 1); P.profile_read()
+for _ in range(3):
+    P.moebius(g, out=y)
+prof, _ = P.profile_read(); P.set_option("profile", 0)
+res["ring8_nostore_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
+P.set_option("ring_debug", 0)
+# int64 data, RING lpe 8
+xi = torch.from_numpy(W.int_values(wl.n, wl.batch, -1000, 1000, seed=3)).cuda()
+gi = P.zeta(xi); yi = torch.empty_like(gi)
+P.moebius(gi, out=yi); torch.cuda.synchronize()
+P.set_option("profile", 1); P.profile_read()
+for _ in range(3):
+    P.moebius(gi, out=yi)
+prof, _ = P.profile_read(); P.set_option("profile", 0)
+res["ring8_i64_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
+res["ok_roundtrip_i64"] = None
+xi = torch.from_numpy(W.int_values(wl.n, 4, -1000, 1000, seed=3)).cuda()
+gi = P.zeta(xi)
+P.set_option("moebius_kernel", pz.MOEB_AUTO)
+res["ok_roundtrip_i64"] = bool(torch.equal(P.moebius(gi), xi))
 print(json.dumps(res))

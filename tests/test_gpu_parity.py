@@ -21,7 +21,7 @@ import paper_2211_13706_b200 as pz  # noqa: E402
 from oracle import brute  # noqa: E402
 from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
 
-KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING, pz.MOEB_CSR]
+KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING, pz.MOEB_CSR, pz.MOEB_RINGWS]
 
 
 def kernels_for(P):
@@ -29,7 +29,8 @@ def kernels_for(P):
     CSR needs the sparse rows, built when RING does not apply)."""
     info = P.info()
     return [k for k in KERNELS
-            if (k != pz.MOEB_RING or info["dist_bytes"] > 0) and (k != pz.MOEB_CSR or info["csr_bytes"] > 0)]
+            if (k != pz.MOEB_RING or info["dist_bytes"] > 0) and (k != pz.MOEB_CSR or info["csr_bytes"] > 0)
+            and (k != pz.MOEB_RINGWS or info["ringws"])]
 facts = load_facts()
 PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
 
@@ -213,13 +214,19 @@ def test_ring_schedule_selection_and_limits():
     P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
     info = P.info()
     assert info["dist_bytes"] > 0 and 0 < info["reach"] < 65535
-    assert info["moebius_kernel"] == pz.MOEB_RING
+    assert info["moebius_kernel"] == pz.MOEB_RINGWS and info["ringws"] == 1
     for B in (1, 2, 7, 33):
         f = W.int_values(n, B, -1000, 1000, seed=B)
         g = gpu_zeta(P, f)
         assert (gpu_moebius(P, g) == f).all(), B
         h = W.int_values(n, B, -10**17, 10**17, seed=B + 9)
-        assert (gpu_moebius(P, h, pz.MOEB_RING) == O.moebius(h)).all(), B
+        want = O.moebius(h)
+        assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), B
+        assert (gpu_moebius(P, h, pz.MOEB_RINGWS) == want).all(), B
+        for lpe in (1, 2, 4, 8, 16):
+            P.set_option("ring_lpe", lpe)
+            assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), (B, lpe)
+        P.set_option("ring_lpe", 8)
     # wide levels (Boolean lattice 2^12: 924-element middle level) do not fit;
     # there AUTO takes the sparse-row schedule
     Pb = pz.Poset(4096, *W.boolean_lattice(12))
@@ -254,6 +261,24 @@ def test_ragged_batches_and_1d():
         assert (gpu_moebius(P, O.zeta(f)) == f).all(), B
     f1 = W.int_values(n, 1, -5, 5, seed=1)[:, 0]
     assert (host(P.zeta(dev(f1))) == O.zeta(f1)).all()
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_dense_gather_variants(variant):
+    """The three dense zeta-gather kernels for batch % 32 == 0 agree with O2
+    (bit-exact int64, tolerance fp64), including a ragged rank tail."""
+    n = 5003
+    src, dst = W.window_dag(n, 2, 64, 7, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    P.set_option("gather_variant", variant)
+    try:
+        for B in (32, 64):
+            f = W.int_values(n, B, -10**15, 10**15, seed=B)
+            assert (gpu_zeta(P, f) == O.zeta(f)).all(), B
+            ff = W.normal_values(n, B, seed=B + 1)
+            assert_fp64_close(gpu_zeta(P, ff), O.zeta(ff), O.zeta(np.abs(ff)))
+    finally:
+        P.set_option("gather_variant", 0)
 
 
 def test_host_buffers_and_inplace():
