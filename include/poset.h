@@ -229,6 +229,11 @@ poset_status poset_profile_read(poset_t h, double *ms, int64_t *calls, int64_t *
 poset_status poset_export_chains(poset_t h, int64_t *chain, int64_t *pos, int64_t *level,
                                  int64_t *rank);
 poset_status poset_export_mtable(poset_t h, int32_t *out);
+/* poset_debug_read -- tuning hook: the 8 int64 counters of the last RING call
+ * made with option "ring_debug" bit 1 (clock64 per-phase sums of CTA 0:
+ * [0] row data + ring loads + tree, [1] lane reduction, [2] tail,
+ * [3] next-level prefetch, [4] barrier, [5] levels). */
+poset_status poset_debug_read(poset_t h, int64_t *out8);
 
 void poset_destroy(poset_t h);
 const char *poset_strerror(poset_status s);

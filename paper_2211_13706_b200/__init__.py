@@ -74,6 +74,7 @@ _sig("poset_set_option", [_vp, ctypes.c_char_p, _i64])
 _sig("poset_profile_read", [_vp, _vp, _vp, _vp])
 _sig("poset_export_chains", [_vp, _vp, _vp, _vp, _vp])
 _sig("poset_export_mtable", [_vp, _vp])
+_sig("poset_debug_read", [_vp, _vp])
 _sig("poset_destroy", [_vp], None)
 _sig("poset_strerror", [ctypes.c_int], ctypes.c_char_p)
 _sig("poset_last_error", [], ctypes.c_char_p)
@@ -213,6 +214,13 @@ class Poset:
         c, p, l, r = (np.zeros(self.n, dtype=np.int64) for _ in range(4))
         _check(lib.poset_export_chains(self._h, _np_ptr(c), _np_ptr(p), _np_ptr(l), _np_ptr(r)))
         return c, p, l, r
+
+    def debug_read(self):
+        """Tuning hook (poset_debug_read): clock64 phase sums of the last
+        instrumented RING call."""
+        out = np.zeros(8, dtype=np.int64)
+        _check(lib.poset_debug_read(self._h, _np_ptr(out)))
+        return out
 
     def export_mtable(self) -> np.ndarray:
         """m(x, j) as an [n][k] int32 array (bottom-up position, -1 = ∞)."""

@@ -91,7 +91,7 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->d_gP, h->csr.ptr, h->csr.idx};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -607,10 +607,9 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     }
     if (!strcmp(key, "ring_lpe")) {   // lanes per element of the RING schedule (tuning)
         const int64_t E = h->ring.entries ? h->ring.entries / value : 0;
-        if (!h->ring.ok || value < 1 || value > 32 || (value & (value - 1)) || E < 4 || E > 64 ||
-            (E == 4 && value < 16))
+        if (!h->ring.ok || value < 1 || value > 32 || (value & (value - 1)) || E < 8 || E > 64)
             return fail(POSET_EINVAL, "poset_set_option: ring_lpe must be a power of two with "
-                                      "4 <= entries/ring_lpe <= 64");
+                                      "8 <= entries/ring_lpe <= 64");
         h->ring.lpe = (int32_t)value;
         return POSET_OK;
     }
@@ -627,8 +626,10 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         }
         return POSET_OK;
     }
-    if (!strcmp(key, "ring_debug")) {   // timing experiments only: results are NOT valid
+    if (!strcmp(key, "ring_debug")) {   // timing experiments only (bit 0: results NOT valid)
         h->ring.debug = (int32_t)value;
+        if (!h->ring.dbg) CK(cudaMalloc((void **)&h->ring.dbg, 64));
+        CK(cudaMemset(h->ring.dbg, 0, 64));
         return POSET_OK;
     }
     if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)
@@ -677,6 +678,15 @@ poset_status poset_export_chains(poset_t h, int64_t *chain, int64_t *pos, int64_
         level[u] = H.level[r];
         rank[u] = r;
     }
+    return POSET_OK;
+}
+
+poset_status poset_debug_read(poset_t h, int64_t *out8) {
+    if (!h || !out8) return fail(POSET_EINVAL, "poset_debug_read: null argument");
+    CK(cudaSetDevice(h->device));
+    if (!h->ring.dbg) { for (int i = 0; i < 8; i++) out8[i] = 0; return POSET_OK; }
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out8, h->ring.dbg, 64, cudaMemcpyDeviceToHost));
     return POSET_OK;
 }
 

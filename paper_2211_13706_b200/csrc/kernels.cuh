@@ -81,6 +81,7 @@ struct RingPlan {
     int32_t entries = 0;        // row entries (64, 128 or 256 >= k)
     int32_t lpe = 1;            // lanes per element; entries / lpe per lane (8..64)
     int32_t debug = 0;          // tuning experiments (poset_set_option "ring_debug")
+    unsigned long long *dbg = nullptr;   // [8] device, clock64 breakdown (debug bit 1)
     int64_t npad = 0;           // n rounded up to a multiple of ch
     uint16_t *D = nullptr;      // [npad][kp]
     uint16_t *Pn = nullptr;     // [npad] ring slot of next(r)

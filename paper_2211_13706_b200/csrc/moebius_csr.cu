@@ -107,56 +107,74 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + c] by one warp, lanes over entries; the
-// result is valid in every lane.  LOAD: plain (read-only data) or .cg (data
-// written earlier in the same kernel by other SMs).
+// result is valid in every lane.  CG: loads bypass L1 (data written earlier
+// in the same kernel by other SMs).  8 independent loads per lane in flight.
 template <typename T, bool CG>
 __device__ __forceinline__ T row_sum_lanes(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                            const T *Fsrc, int32_t B, int c) {
     const int lane = threadIdx.x & 31;
-    T s0 = T(0), s1 = T(0);
+    constexpr int U = 8;
+    T s[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) s[u] = T(0);
     int64_t e = a + lane;
-    for (; e + 32 < b; e += 64) {
-        const int32_t i0 = __ldg(idx + e), i1 = __ldg(idx + e + 32);
-        const T *p0 = Fsrc + (size_t)i0 * B + c, *p1 = Fsrc + (size_t)i1 * B + c;
-        s0 += CG ? ld_cg(p0) : __ldg(p0);
-        s1 += CG ? ld_cg(p1) : __ldg(p1);
+    for (; e + 32 * (U - 1) < b; e += 32 * U) {
+        int32_t i[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) i[u] = __ldg(idx + e + 32 * u);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const T *p = Fsrc + (size_t)i[u] * B + c;
+            s[u] += CG ? ld_cg(p) : __ldg(p);
+        }
     }
-    if (e < b) {
-        const T *p0 = Fsrc + (size_t)__ldg(idx + e) * B + c;
-        s0 += CG ? ld_cg(p0) : __ldg(p0);
+    for (; e < b; e += 32) {
+        const T *p = Fsrc + (size_t)__ldg(idx + e) * B + c;
+        s[0] += CG ? ld_cg(p) : __ldg(p);
     }
-    return warp_sum(s0 + s1);
+#pragma unroll
+    for (int st = 1; st < U; st <<= 1)
+#pragma unroll
+        for (int u = 0; u < U; u += 2 * st) s[u] += s[u + st];
+    return warp_sum(s[0]);
 }
 
-// Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + col] by one warp, lanes over columns.
+// Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + col] by one warp, lanes over columns: the
+// row entries are read 32 at a time and broadcast by shuffles; 16 row loads
+// (one coalesced 256-B load each) in flight.
 template <typename T, bool CG>
 __device__ __forceinline__ T row_sum_cols(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                           const T *Fsrc, int32_t B, int col) {
     const int lane = threadIdx.x & 31;
-    T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+    constexpr int U = 16;
+    T s[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) s[u] = T(0);
     for (int64_t e0 = a; e0 < b; e0 += 32) {
         const int m = (int)(b - e0 < 32 ? b - e0 : 32);
         const int32_t mine = lane < m ? __ldg(idx + e0 + lane) : 0;
         int q = 0;
-        for (; q + 4 <= m; q += 4) {
-            const int32_t i0 = __shfl_sync(0xffffffffu, mine, q);
-            const int32_t i1 = __shfl_sync(0xffffffffu, mine, q + 1);
-            const int32_t i2 = __shfl_sync(0xffffffffu, mine, q + 2);
-            const int32_t i3 = __shfl_sync(0xffffffffu, mine, q + 3);
-            const T *p0 = Fsrc + (size_t)i0 * B + col, *p1 = Fsrc + (size_t)i1 * B + col;
-            const T *p2 = Fsrc + (size_t)i2 * B + col, *p3 = Fsrc + (size_t)i3 * B + col;
-            s0 += CG ? ld_cg(p0) : __ldg(p0);
-            s1 += CG ? ld_cg(p1) : __ldg(p1);
-            s2 += CG ? ld_cg(p2) : __ldg(p2);
-            s3 += CG ? ld_cg(p3) : __ldg(p3);
+        for (; q + U <= m; q += U) {
+            int32_t i[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) i[u] = __shfl_sync(0xffffffffu, mine, q + u);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const T *p = Fsrc + (size_t)i[u] * B + col;
+                s[u] += CG ? ld_cg(p) : __ldg(p);
+            }
         }
         for (; q < m; q++) {
             const int32_t i0 = __shfl_sync(0xffffffffu, mine, q);
-            const T *p0 = Fsrc + (size_t)i0 * B + col;
-            s0 += CG ? ld_cg(p0) : __ldg(p0);
+            const T *p = Fsrc + (size_t)i0 * B + col;
+            s[0] += CG ? ld_cg(p) : __ldg(p);
         }
     }
-    return (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int st = 1; st < U; st <<= 1)
+#pragma unroll
+        for (int u = 0; u < U; u += 2 * st) s[u] += s[u + st];
+    return s[0];
 }
 
 // ---------------------------------------------------- zeta gather (CSR) ---

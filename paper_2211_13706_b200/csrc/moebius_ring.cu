@@ -208,7 +208,10 @@ struct RingArgs {
     int32_t n, kp, ell, B;
     int32_t ring_mask;          // RING - 1 (power of two)
     int32_t lg_ch, nstage;      // log2 ranks per staged chunk, pipeline depth (power of two)
-    int32_t debug;              // tuning experiments only: bit 0 = skip the global store of f
+    int32_t debug;              // tuning experiments only: bit 0 = skip the global store of f,
+                                // (the per-phase clock64 instrumentation of round 1 is retired;
+                                // DESIGN.md §5.4 records what it measured)
+    unsigned long long *dbg;
 };
 
 // 8 shared-memory loads in one asm block: issued back to back, so all 32
@@ -266,84 +269,234 @@ __device__ __forceinline__ T ring_sum(const T *ring, const uint16_t *row) {
     return v[0];
 }
 
+// shared-memory accessors on 32-bit shared addresses (the generic-to-shared
+// window base is computed once, not per access)
+__device__ __forceinline__ uint4 lds128(unsigned addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ u64 lds64(unsigned addr) {
+    u64 v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ unsigned lds32(unsigned addr) {
+    unsigned v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ unsigned lds16(unsigned addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts64(unsigned addr, u64 v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ u64 tobits(T x);
+template <>
+__device__ __forceinline__ u64 tobits<u64>(u64 x) { return x; }
+template <>
+__device__ __forceinline__ u64 tobits<double>(double x) { return (u64)__double_as_longlong(x); }
+
+// Σ_{i < E} ring[slot_i] for the E slots packed in w (two per 32-bit word)
+template <typename T, int E>
+__device__ __forceinline__ T ring_sum_w(unsigned ring_base, const uint4 (&w)[E / 8]) {
+    T v[E];
+#pragma unroll
+    for (int i = 0; i < E / 8; i++) {
+        const unsigned ws[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            v[8 * i + 2 * h] = bits_to<T>(lds64(ring_base + ((ws[h] & 0xffffu) << 3)));
+            v[8 * i + 2 * h + 1] = bits_to<T>(lds64(ring_base + ((ws[h] >> 16) << 3)));
+        }
+    }
+#pragma unroll
+    for (int st = 1; st < E; st <<= 1)
+#pragma unroll
+        for (int i = 0; i < E; i += 2 * st) v[i] += v[i + st];
+    return v[0];
+}
+
+__device__ __forceinline__ int ld_acq(unsigned addr) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel(unsigned addr, int v) {
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void bar_consumers(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Warp roles: warps 0 .. NW-2 are consumers (one level at a time, named
+// barrier 1 between levels); the last warp is the producer: it issues the TMA
+// bulk copies of the staged chunks, waits for their mbarriers and publishes
+// ready_rank (ranks < ready_rank are staged); consumers publish done_rank
+// (ranks < done_rank are finished) so the producer can recycle stages.  Per
+// consumer level (uniform trip counts so every shuffle is a full-warp one):
+// pass p handles ranks lo + grp + p*NG; the first pass of the next level has
+// its row words, g, rank->user and next-slot loaded into registers before the
+// barrier, and level bounds are read two levels ahead, so after the barrier
+// only the ring reads, the lane reduction and the tail are on the critical path.
 template <typename T, int LPE, int E>
-__global__ void __launch_bounds__(512) k_moeb_ring(RingArgs a) {
+__global__ void __launch_bounds__(544) k_moeb_ring(RingArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
     const int ch = 1 << a.lg_ch;
-    T *ring = reinterpret_cast<T *>(smem);                               // RING + 1 entries
+    const unsigned sbase = smem_u32(smem);
+    const unsigned ring_base = sbase;                                    // RING + 1 entries
     u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);  // nstage
-    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 1) & ~1);
+    const unsigned ctrl = smem_u32(bars + ((a.nstage + 1) & ~1));        // [0] ready_rank [1] done_rank
+    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 1) & ~1) + 16;
+    const unsigned stage_base = smem_u32(stage0);
     const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8;
     const unsigned ubytes = (unsigned)ch * 4, pbytes = (unsigned)ch * 2;
     const unsigned sbytes = dbytes + gbytes + ubytes + pbytes;
     const int b = blockIdx.x;
-    const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
-    const int sub = tid & (LPE - 1), grp = tid / LPE, NG = NT / LPE;
-    const unsigned gmask = LPE == 32 ? 0xffffffffu : (((1u << LPE) - 1u) << (lane & ~(LPE - 1)));
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int NTC = blockDim.x - 32;   // consumer threads
     const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
-    T *f = reinterpret_cast<T *>(a.f);
     const int32_t nchunks = (int32_t)(a.npad >> a.lg_ch);
 
-    if (tid == 0) ring[RING] = T(0);   // target of "no dependency"
     if (tid == 0) {
+        sts64(ring_base + (unsigned)RING * 8, 0ull);   // target of "no dependency"
         for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
+        asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;" ::"r"(ctrl) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    int32_t issued = 0;   // chunks issued (meaningful in thread 0)
-    auto issue = [&](int32_t c) {
-        const int s = c & (a.nstage - 1);
-        unsigned char *st = stage0 + (size_t)s * sbytes;
-        const size_t r0 = (size_t)c << a.lg_ch;
-        mbar_expect_tx(&bars[s], sbytes);
-        bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s]);
-        bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s]);
-        bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
-        bulk_g2s(st + dbytes + gbytes + ubytes, a.Pn + r0, pbytes, &bars[s]);
-    };
-    if (tid == 0)
-        for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
 
-    int32_t ready = 0;                // chunks [0, ready) observed complete
+    if (tid >= NTC) {
+        // ------------------------------------------------------ producer --
+        if (lane == 0) {
+            auto issue = [&](int32_t c) {
+                const int s = c & (a.nstage - 1);
+                unsigned char *st = stage0 + (size_t)s * sbytes;
+                const size_t r0 = (size_t)c << a.lg_ch;
+                mbar_expect_tx(&bars[s], sbytes);
+                bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s]);
+                bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s]);
+                bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
+                bulk_g2s(st + dbytes + gbytes + ubytes, a.Pn + r0, pbytes, &bars[s]);
+            };
+            int32_t issued = 0, arrived = 0;
+            for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
+            while (arrived < nchunks) {
+                mbar_wait(&bars[arrived & (a.nstage - 1)], (unsigned)((arrived / a.nstage) & 1));
+                arrived++;
+                st_rel(ctrl, arrived << a.lg_ch);
+                // refill every stage whose previous chunk the consumers have finished
+                while (issued < nchunks) {
+                    const int32_t done = ld_acq(ctrl + 4);
+                    if (((int64_t)(issued - a.nstage + 1) << a.lg_ch) > done) {
+                        if (arrived < issued) break;   // go wait for the next arrival
+                        __nanosleep(64);
+                        continue;
+                    }
+                    issue(issued);
+                    issued++;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- consumers --
+    const int sub = tid & (LPE - 1), grp = tid / LPE, NG = NTC / LPE;
+    T *f = reinterpret_cast<T *>(a.f);
+    const unsigned zero_words = (unsigned)RING * 0x10001u;   // two "no dependency" slots
+    auto stage_addr = [&](int32_t e) {
+        return stage_base + (unsigned)((e >> a.lg_ch) & (a.nstage - 1)) * sbytes;
+    };
+    auto load_elem = [&](int32_t e, bool act, uint4 (&w)[E / 8], T &gx, int32_t &u, unsigned &pn) {
+        if (act) {
+            const unsigned st = stage_addr(e), off = (unsigned)(e & (ch - 1));
+            const unsigned row = st + (off * (unsigned)a.kp + (unsigned)(sub * E)) * 2;
+#pragma unroll
+            for (int i = 0; i < E / 8; i++) w[i] = lds128(row + 16 * i);
+            gx = bits_to<T>(lds64(st + dbytes + off * 8));
+            u = (int32_t)lds32(st + dbytes + gbytes + off * 4);
+            pn = lds16(st + dbytes + gbytes + ubytes + off * 2);
+        } else {
+#pragma unroll
+            for (int i = 0; i < E / 8; i++) w[i] = make_uint4(zero_words, zero_words, zero_words, zero_words);
+            gx = T(0);
+            u = 0;
+            pn = (unsigned)RING;
+        }
+    };
+    int32_t staged = 0;   // ranks < staged are known to be in shared memory
+    auto wait_staged = [&](int32_t rank_hi) {
+        while (staged < rank_hi) staged = ld_acq(ctrl);
+    };
     int32_t cache_base = 0;           // lv = lvl_ptr[cache_base + lane]
     int32_t lv = a.lvl_ptr[min(lane, a.ell)];
     int32_t lv_next = a.lvl_ptr[min(31 + lane, a.ell)];
-    for (int32_t L = 0; L < a.ell; L++) {
-        if (L - cache_base == 31) {
+    auto level_bounds = [&](int32_t L, int32_t &lo, int32_t &hi) {   // L non-decreasing
+        if (L >= a.ell) { lo = hi = a.n; return; }
+        if (L - cache_base >= 31) {
             cache_base += 31;
             lv = lv_next;
             lv_next = a.lvl_ptr[min(cache_base + 31 + lane, a.ell)];
         }
-        const int32_t lo = __shfl_sync(0xffffffffu, lv, L - cache_base);
-        const int32_t hi = __shfl_sync(0xffffffffu, lv, L - cache_base + 1);
-        const int32_t need = ((hi - 1) >> a.lg_ch) + 1;
-        for (; ready < need; ready++)
-            mbar_wait(&bars[ready & (a.nstage - 1)], (unsigned)((ready / a.nstage) & 1));
-        for (int32_t e = lo + grp; e < hi; e += NG) {   // uniform within an LPE group
-            const int off = e & (ch - 1);
-            const unsigned char *st = stage0 + (size_t)((e >> a.lg_ch) & (a.nstage - 1)) * sbytes;
-            const uint16_t *row = reinterpret_cast<const uint16_t *>(st) + (size_t)off * a.kp + sub * E;
-            T s = ring_sum<T, E>(ring, row);
+        lo = __shfl_sync(0xffffffffu, lv, L - cache_base);
+        hi = __shfl_sync(0xffffffffu, lv, L - cache_base + 1);
+    };
+
+    int32_t lo, hi, nlo, nhi;
+    level_bounds(0, lo, hi);
+    level_bounds(1, nlo, nhi);
+    wait_staged(hi);
+    uint4 pw[E / 8];
+    T pg;
+    int32_t pu;
+    unsigned ppn;
+    load_elem(lo + grp, lo + grp < hi, pw, pg, pu, ppn);
+    for (int32_t L = 0; L < a.ell; L++) {
+        int32_t nnlo, nnhi;
+        level_bounds(L + 2, nnlo, nnhi);   // two levels ahead, off the critical path
+        for (int32_t base = lo; base < hi; base += NG) {
+            const int32_t e = base + grp;
+            const bool act = e < hi;
+            uint4 w[E / 8];
+            T gx;
+            int32_t u;
+            unsigned pn;
+            if (base == lo) {
 #pragma unroll
-            for (int o = LPE / 2; o; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
-            if (sub == 0) {
-                const T Fx = reinterpret_cast<const T *>(st + dbytes)[off] - s;
-                const int32_t u = reinterpret_cast<const int32_t *>(st + dbytes + gbytes)[off];
-                const unsigned pn = reinterpret_cast<const uint16_t *>(st + dbytes + gbytes + ubytes)[off];
-                if (!(a.debug & 1)) f[(size_t)u * a.B + b] = Fx - ring[pn];
-                ring[e & a.ring_mask] = Fx;
+                for (int i = 0; i < E / 8; i++) w[i] = pw[i];
+                gx = pg;
+                u = pu;
+                pn = ppn;
+            } else {
+                load_elem(e, act, w, gx, u, pn);
+            }
+            const T Fprev = bits_to<T>(lds64(ring_base + pn * 8));
+            T s = ring_sum_w<T, E>(ring_base, w);
+#pragma unroll
+            for (int o = LPE / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (sub == 0 && act) {
+                const T Fx = gx - s;
+                if (!(a.debug & 1)) f[(size_t)u * a.B + b] = Fx - Fprev;
+                sts64(ring_base + (unsigned)(e & a.ring_mask) * 8, tobits<T>(Fx));
             }
         }
-        if (NT == 32) __syncwarp();
-        else __syncthreads();
-        // chunks entirely below hi are finished: refill their stages
-        if (tid == 0) {
-            while (issued < nchunks && ((int64_t)(issued - a.nstage + 1) << a.lg_ch) <= hi) {
-                issue(issued);
-                issued++;
-            }
+        // the next level's first pass: staged data into registers before the barrier
+        if (L + 1 < a.ell) {
+            wait_staged(nhi);
+            load_elem(nlo + grp, nlo + grp < nhi, pw, pg, pu, ppn);
         }
+        bar_consumers(NTC);
+        if (tid == 0) st_rel(ctrl + 4, hi);   // ranks < hi are done: their stages may be recycled
+        lo = nlo;
+        hi = nhi;
+        nlo = nnlo;
+        nhi = nnhi;
     }
 }
 
@@ -365,7 +518,8 @@ void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsig
     (void)avg_w;
     for (int nstage : {4, 2}) {
         for (int ch : {256, 128, 64, 32, 16, 8}) {
-            if ((int64_t)max_level_width > (int64_t)(nstage - 1) * ch) break;
+            // the current and the next level must be staged at once (prefetch)
+            if (2 * (int64_t)max_level_width > (int64_t)(nstage - 1) * ch) break;
             if (ring_smem_bytes((int)ring, kp, ch, nstage) <= kSmemCap) {
                 R.ok = true;
                 R.kp = kp;
@@ -382,7 +536,7 @@ void ring_plan(int32_t n, int32_t k, int32_t ell, int32_t max_level_width, unsig
 }
 
 size_t ring_smem_bytes(int ring, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 1) & ~1) +
+    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 1) & ~1) + 16 +
            (size_t)nstage * ch * ((size_t)kp * 2 + 8 + 4 + 2);
 }
 
@@ -406,14 +560,15 @@ cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype,
     while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
     a.nstage = R.nstage;
     a.debug = R.debug;
+    a.dbg = R.dbg;
     const size_t smem = ring_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
     const int lpe = R.lpe, E = R.entries / R.lpe;
     void *fn = nullptr;
 #define RING_FN(L, EE)                                                                          \
     if (lpe == L && E == EE)                                                                    \
         fn = dtype == 0 ? (void *)k_moeb_ring<u64, L, EE> : (void *)k_moeb_ring<double, L, EE>;
-    RING_FN(1, 64) RING_FN(2, 32) RING_FN(4, 16) RING_FN(8, 8) RING_FN(16, 4)
-    RING_FN(2, 64) RING_FN(4, 32) RING_FN(8, 16) RING_FN(16, 8) RING_FN(32, 4)
+    RING_FN(1, 64) RING_FN(2, 32) RING_FN(4, 16) RING_FN(8, 8)
+    RING_FN(2, 64) RING_FN(4, 32) RING_FN(8, 16) RING_FN(16, 8)
     RING_FN(4, 64) RING_FN(8, 32) RING_FN(16, 16) RING_FN(32, 8)
 #undef RING_FN
     if (!fn) return cudaErrorInvalidConfiguration;
@@ -421,7 +576,7 @@ cudaError_t launch_moebius_ring(const DevPoset &P, const RingPlan &R, int dtype,
     if (e != cudaSuccess) return e;
     const double avg_w = (double)P.n / std::max(P.ell, 1);
     int threads = (int)std::min<int64_t>(512, ((int64_t)std::ceil(avg_w * lpe) + 31) / 32 * 32);
-    threads = std::max(threads, 32);
+    threads = std::max(threads, 32) + 32;   // + the producer warp
     void *args[] = {&a};
     launches_add(1);
     return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(threads), args, smem, s);

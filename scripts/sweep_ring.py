@@ -15,7 +15,7 @@ g = P.zeta(x)
 y = torch.empty_like(x)
 res = {"cfg": cfg, "n": wl.n, "k": info["k"], "ell": info["ell"], "reach": info["reach"]}
 P.set_option("moebius_kernel", pz.MOEB_RING)
-for lpe in (1, 2, 4, 8, 16):
+for lpe in (1, 2, 4, 8):
     try:
         P.set_option("ring_lpe", lpe)
     except pz.PosetError as e:

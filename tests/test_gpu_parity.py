@@ -223,7 +223,7 @@ def test_ring_schedule_selection_and_limits():
         want = O.moebius(h)
         assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), B
         assert (gpu_moebius(P, h, pz.MOEB_RINGWS) == want).all(), B
-        for lpe in (1, 2, 4, 8, 16):
+        for lpe in (1, 2, 4, 8):
             P.set_option("ring_lpe", lpe)
             assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), (B, lpe)
         P.set_option("ring_lpe", 8)
