@@ -352,8 +352,10 @@ void ringws_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
                 R.ch = ch;
                 R.nstage = nstage;
                 R.npad = ((int64_t)n + ch - 1) / ch * ch;
-                R.lpeo = std::min(32, fe / 8);   // 8 far entries per lane
-                R.nwo = 8;
+                // 16 far entries per lane, 4 old warps: the best of the
+                // (nwo, lpeo) sweep on C5w (profiles/r1_ring_notes.md)
+                R.lpeo = std::min(32, std::max(4, fe / 16));
+                R.nwo = 4;
                 return;
             }
         }
