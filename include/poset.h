@@ -75,9 +75,12 @@ typedef enum {
                                  ring, U-solve and chain difference fused   */
     POSET_MOEB_CSR = 5,       /* sparse U-rows, persistent kernel with a grid barrier per
                                  level, one warp per (element, column group) */
-    POSET_MOEB_RINGWS = 6     /* RING with warp specialisation: one warp on the level-by-level
+    POSET_MOEB_RINGWS = 6,    /* RING with warp specialisation: one warp on the level-by-level
                                  critical path (near dependencies only), the others summing the
                                  far dependencies ahead of it                 */
+    POSET_MOEB_RINGDF = 7     /* barrier-free level pipeline: warps own levels round-robin and
+                                 sync through one levels-done counter; far / mid dependencies
+                                 are summed levels ahead, near ones on the critical path     */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -104,6 +107,7 @@ typedef struct {
     int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
     int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
+    int64_t ringdf;       /* 1 if the RINGDF schedule is available                  */
 } poset_info;
 
 /*

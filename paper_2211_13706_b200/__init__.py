@@ -23,7 +23,8 @@ import os
 import numpy as np
 
 __all__ = ["Poset", "PosetError", "analyze", "lib", "MOEB_AUTO", "MOEB_LEVEL", "MOEB_GRID", "MOEB_WARP",
-           "MOEB_RING", "MOEB_CSR", "MOEB_RINGWS", "LIB_PATH"]
+           "MOEB_RING", "MOEB_CSR", "MOEB_RINGWS", "MOEB_RINGDF",
+           "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposet.so")
 
@@ -35,7 +36,8 @@ try:
 except OSError as e:   # pragma: no cover
     raise ImportError(f"cannot load {LIB_PATH}: {e} (there is no CPU fallback)") from e
 
-MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS = 0, 1, 2, 3, 4, 5, 6
+MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS, MOEB_RINGDF = (
+    0, 1, 2, 3, 4, 5, 6, 7)
 _I64, _F64 = 0, 1
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -49,7 +51,7 @@ class PosetInfo(ctypes.Structure):
                 ("t_upload", ctypes.c_double), ("t_mtable", ctypes.c_double),
                 ("device", ctypes.c_int32), ("moebius_kernel", ctypes.c_int32),
                 ("reach", _i64), ("dist_bytes", _i64), ("t_dist", ctypes.c_double),
-                ("csr_bytes", _i64), ("zeta_sparse", _i64), ("ringws", _i64)]
+                ("csr_bytes", _i64), ("zeta_sparse", _i64), ("ringws", _i64), ("ringdf", _i64)]
 
 
 def _sig(name, args, res=ctypes.c_int):

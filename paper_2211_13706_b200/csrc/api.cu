@@ -38,6 +38,7 @@ struct poset_s {
     unsigned long long *d_count = nullptr;
     RingPlan ring;                    // RING Möbius schedule (moebius_ring.cu)
     RingWSPlan rws;                   // RINGWS Möbius schedule (moebius_ringws.cu)
+    RingDFPlan rdf;                   // RINGDF Möbius schedule (moebius_ringdf.cu)
     CsrRows csr;                      // sparse U-rows (moebius_csr.cu)
     bool zeta_csr = false;            // zeta gathers over the CSR rows (sparse table)
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
@@ -91,7 +92,7 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -150,17 +151,21 @@ static poset_status finish_setup(poset_s *h) {
         int32_t *d_slot_rank = nullptr, *d_level = nullptr;
         CK(upload(&d_slot_rank, H.slot_rank));
         CK(upload(&d_level, H.level));
-        unsigned reach = 0, near3[3] = {0, 0, 0};
+        unsigned reach = 0, near3[3] = {0, 0, 0}, counts2[2] = {0, 0};
         cudaError_t e = launch_reach_max(P, d_slot_rank, (unsigned *)h->d_count, 0);
         if (e == cudaSuccess) e = cudaMemcpy(&reach, h->d_count, sizeof reach, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess) e = launch_near_max(P, d_level, d_slot_rank, (unsigned *)h->d_count, 0);
         if (e == cudaSuccess) e = cudaMemcpy(near3, h->d_count, sizeof near3, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = launch_df_counts(P, d_level, d_slot_rank, (unsigned *)h->d_count, 0);
+        if (e == cudaSuccess) e = cudaMemcpy(counts2, h->d_count, sizeof counts2, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) { cudaFree(d_slot_rank); cudaFree(d_level); CK(e); }
         ring_plan(H.n, H.k, H.ell, H.max_level_width, reach, h->ring);
         ringws_plan(H.n, H.k, H.max_level_width, reach, near3, h->rws);
-        const int64_t npad = ((int64_t)H.n + 255) / 256 * 256;   // common to both plans
+        ringdf_plan(H.n, H.k, H.max_level_width, reach, counts2, h->rdf);
+        const int64_t npad = ((int64_t)H.n + 255) / 256 * 256;   // common to all plans
         h->ring.npad = npad;
         h->rws.npad = npad;
+        h->rdf.npad = npad;
         size_t fb = 0, tb = 0;
         cudaMemGetInfo(&fb, &tb);
         const size_t reserve = (size_t)1 << 30;
@@ -169,16 +174,18 @@ static poset_status finish_setup(poset_s *h) {
             fb -= bytes;
             return true;
         };
-        if ((h->ring.ok || h->rws.ok) && !alloc((void **)&h->ring.ru_pad, (size_t)npad * 4)) {
+        if ((h->ring.ok || h->rws.ok || h->rdf.ok) && !alloc((void **)&h->ring.ru_pad, (size_t)npad * 4)) {
             h->ring.ok = false;
             h->rws.ok = false;
+            h->rdf.ok = false;
         }
+        if (h->rdf.ok && !alloc((void **)&h->rdf.D, (size_t)npad * h->rdf.kp * 2)) h->rdf.ok = false;
         if (h->ring.ok && !(alloc((void **)&h->ring.D, (size_t)npad * h->ring.kp * 2) &&
                             alloc((void **)&h->ring.Pn, (size_t)npad * 2)))
             h->ring.ok = false;
         if (h->rws.ok && !alloc((void **)&h->rws.D, (size_t)npad * h->rws.kp * 2)) h->rws.ok = false;
         e = cudaSuccess;
-        if (h->ring.ok || h->rws.ok) {
+        if (h->ring.ok || h->rws.ok || h->rdf.ok) {
             e = cudaMemset(h->ring.ru_pad, 0, (size_t)npad * 4);
             if (e == cudaSuccess)
                 e = cudaMemcpy(h->ring.ru_pad, h->d_rank_user, (size_t)H.n * 4, cudaMemcpyDeviceToDevice);
@@ -186,6 +193,7 @@ static poset_status finish_setup(poset_s *h) {
         if (e == cudaSuccess && h->ring.ok)
             e = launch_build_dist(P, d_slot_rank, h->ring.kp, h->ring.ring, npad, h->ring.D, h->ring.Pn, 0);
         if (e == cudaSuccess && h->rws.ok) e = launch_build_ringws(P, h->rws, d_level, d_slot_rank, 0);
+        if (e == cudaSuccess && h->rdf.ok) e = launch_build_ringdf(P, h->rdf, d_level, d_slot_rank, 0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         cudaFree(d_slot_rank);
         cudaFree(d_level);
@@ -221,12 +229,15 @@ static poset_status finish_setup(poset_s *h) {
     I.device = h->device;
     I.reach = h->ring.reach;
     I.dist_bytes = (h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0) +
-                   (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0);
+                   (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0) +
+                   (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
+    I.ringdf = h->rdf.ok ? 1 : 0;
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
-    I.moebius_kernel = h->rws.ok   ? MOEB_RINGWS
+    I.moebius_kernel = h->rdf.ok   ? MOEB_RINGDF
+                       : h->rws.ok   ? MOEB_RINGWS
                        : h->ring.ok  ? MOEB_RING
                        : h->csr.ok ? MOEB_CSR
                                    : moebius_pick(P, 1, H.max_level_width, h->num_sms);
@@ -389,6 +400,7 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
     if (st) return st;
     DevPoset P = h->dev();
     int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
+                : h->rdf.ok  ? MOEB_RINGDF
                 : h->rws.ok  ? MOEB_RINGWS
                 : h->ring.ok ? MOEB_RING
                 : h->csr.ok  ? MOEB_CSR
@@ -402,6 +414,19 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
+    if (which == MOEB_RINGDF) {
+        if (!h->rdf.ok)
+            return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
+        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
+        if (st) return st;
+        {
+            PhaseTimer t(h, POSET_PH_PERM, s);
+            CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
+        }
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+        return POSET_OK;
+    }
     if (which == MOEB_RINGWS) {
         if (!h->rws.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGWS schedule does not fit this poset; use AUTO");
@@ -601,7 +626,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_RINGWS) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RINGDF) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }

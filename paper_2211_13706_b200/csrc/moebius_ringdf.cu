@@ -1,0 +1,437 @@
+// Kernel (v), schedule RINGDF: barrier-free level pipeline for the Möbius
+// solve of bounded-reach posets (C5w) -- NEXT row N2, DESIGN.md §5.4.
+//
+// Alg. 4: F(x) = g(x) - Σ_{j ≠ id(x)} F(niv_j(x)),
+// f(x) = F(x) - F(next(x)), swept over the antichain levels (Alg. 6,
+// P:L709-733; Alg. 5 P:L692-705 puts a barrier between levels).
+//
+// Here there is no barrier.  One CTA per column; consumer warp w owns the
+// levels L ≡ w (mod NWC), one lane per element.  A single shared counter
+// `levels_done` (levels < levels_done are finished; it advances in level
+// order) replaces the barrier.  The dependencies of an element of level L are
+// split by their own level when the tables are built:
+//   far   level <= L - 7   summed once levels_done >= L - 6
+//   mid   level in [L-6, L-3]   summed once levels_done >= L - 2
+//   near  level >= L - 2   (at most NN) summed once levels_done >= L
+// so while the other warps finish levels L-6 .. L-1, warp w has already done
+// almost all of its work for level L; what remains on the critical path of a
+// level is one poll of levels_done, <= NN shared-memory loads, a few adds, the
+// ring store and the release of levels_done.  The ring of F values, the
+// TMA-staged rows (producer warp) and the sizes follow RING; the plan makes
+// RING >= reach + 12 * max level width so no slot is overwritten while any
+// warp may still read it.
+//
+//   rows [npad][kp] uint16 ring slots (RING = the zero entry):
+//     [0, NN) near | [NN, NN+NM) mid | [NN+NM, NN+NM+FE) far (bank-sorted) | pn
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace poset {
+
+typedef unsigned long long u64;
+
+static constexpr int kNear = 2;    // level distance <= kNear: near
+static constexpr int kMid = 6;     // kNear < distance <= kMid: mid; beyond: far
+static constexpr int kNWC = 8;     // consumer warps per CTA
+
+// ------------------------------------------------------------ setup -------
+// max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
+__global__ void k_df_counts(const int32_t *__restrict__ M, int32_t n, int32_t k,
+                            const int32_t *__restrict__ chain, const int32_t *__restrict__ level,
+                            const int32_t *__restrict__ slot_rank, unsigned *out2) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned cn = 0, cm = 0;
+    if (r < n) {
+        const int32_t own = chain[r], lr = level[r];
+        for (int32_t j = 0; j < k; j++) {
+            const int32_t s = __ldcs(M + (size_t)j * n + r);
+            if (j == own || s == n) continue;
+            const int32_t ld = lr - level[slot_rank[s]];
+            cn += ld <= kNear;
+            cm += ld > kNear && ld <= kMid;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        cn = max(cn, __shfl_xor_sync(0xffffffffu, cn, o));
+        cm = max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out2, cn);
+        atomicMax(out2 + 1, cm);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_build_ringdf(
+    const int32_t *__restrict__ M, int32_t n, int32_t k, int32_t kp, int32_t nn, int32_t nm,
+    int32_t fe, int32_t ring, const int32_t *__restrict__ chain, const int32_t *__restrict__ slot,
+    const int32_t *__restrict__ slot_rank, const int32_t *__restrict__ level,
+    uint16_t *__restrict__ D) {
+    extern __shared__ uint16_t tile[];   // raw [32][k+1] slots, class [32][k+1], out [32][kp]
+    const int ks = k + 1;
+    uint16_t *raw = tile, *cls = tile + 32 * ks, *outr = tile + 64 * ks;
+    const int r0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int r = r0 + lane;
+    const int mask = ring - 1;
+    for (int j = w; j < k; j += nw) {
+        int dep = -1;
+        if (r < n) {
+            const int32_t s = M[(size_t)j * n + r];
+            if (s != n && chain[r] != j) dep = slot_rank[s];
+        }
+        raw[lane * ks + j] = (uint16_t)(dep >= 0 ? (dep & mask) : ring);
+        int c = 3;   // 0 near, 1 mid, 2 far, 3 none
+        if (dep >= 0) {
+            const int32_t ld = level[r] - level[dep];
+            c = ld <= kNear ? 0 : ld <= kMid ? 1 : 2;
+        }
+        cls[lane * ks + j] = (uint16_t)c;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const uint16_t *in = raw + lane * ks, *cl = cls + lane * ks;
+        uint16_t *out = outr + lane * kp;
+        int nnear = 0, nmid = 0, cnt[16], pos[16], acc = 0;
+#pragma unroll
+        for (int c = 0; c < 16; c++) cnt[c] = 0;
+        for (int j = 0; j < k; j++) {
+            const int s = in[j];
+            if (cl[j] == 0) { if (nnear < nn) out[nnear] = (uint16_t)s; nnear++; }
+            else if (cl[j] == 1) { if (nmid < nm) out[nn + nmid] = (uint16_t)s; nmid++; }
+            else if (cl[j] == 2) cnt[(s - r) & 15]++;
+        }
+        for (int j = nnear; j < nn; j++) out[j] = (uint16_t)ring;
+        for (int j = nmid; j < nm; j++) out[nn + j] = (uint16_t)ring;
+#pragma unroll
+        for (int c = 0; c < 16; c++) { pos[c] = acc; acc += cnt[c]; }
+        for (int j = 0; j < k; j++) {
+            if (cl[j] != 2) continue;
+            const int s = in[j];
+            const int c = (s - r) & 15;
+#pragma unroll
+            for (int cc = 0; cc < 16; cc++)
+                if (cc == c) out[nn + nm + pos[cc]++] = (uint16_t)s;
+        }
+        for (int j = nn + nm + acc; j < kp; j++) out[j] = (uint16_t)ring;
+        int pn = -1;
+        if (r < n) {
+            const int32_t s = slot[r];
+            if (s > 0) {
+                const int32_t p = slot_rank[s - 1];
+                if (chain[p] == chain[r]) pn = p;
+            }
+        }
+        out[nn + nm + fe] = (uint16_t)(pn >= 0 ? (pn & mask) : ring);
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)r0 * kp;
+    for (int t = threadIdx.x; t < 32 * kp; t += blockDim.x) D[base + t] = outr[t];
+}
+
+// ------------------------------------------------------------ kernel ------
+struct RDFArgs {
+    const uint16_t *D;          // [npad][kp]
+    const void *gP;             // [B][npad]
+    const int32_t *ru;          // [npad]
+    const int32_t *lvl_ptr;     // [ell + 1]
+    void *f;                    // [n][B]
+    int64_t npad;
+    int32_t n, kp, ell, B;
+    int32_t ring_mask;
+    int32_t lg_ch, nstage;
+};
+
+__device__ __forceinline__ uint4 df_lds128(unsigned addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ u64 df_lds64(unsigned addr) {
+    u64 v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ int df_acq(unsigned addr) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void df_rel(unsigned addr, int v) {
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// Σ ring[slot] over E consecutive row words at shared address `row`
+template <typename T, int E>
+__device__ __forceinline__ T df_sum(unsigned ring_base, unsigned row) {
+    static_assert(E == 8 || E % 16 == 0, "row segments are 8 or a multiple of 16 entries");
+    T acc = T(0);
+    if constexpr (E == 8) {
+        const uint4 w0 = df_lds128(row);
+        const unsigned ws[4] = {w0.x, w0.y, w0.z, w0.w};
+        T v[8];
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            v[2 * h] = bits_to<T>(df_lds64(ring_base + ((ws[h] & 0xffffu) << 3)));
+            v[2 * h + 1] = bits_to<T>(df_lds64(ring_base + ((ws[h] >> 16) << 3)));
+        }
+        return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+    }
+#pragma unroll
+    for (int c = 0; c < E; c += 16) {
+        const uint4 w0 = df_lds128(row + 2 * c), w1 = df_lds128(row + 2 * c + 16);
+        const unsigned ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        T v[16];
+#pragma unroll
+        for (int h = 0; h < 8; h++) {
+            v[2 * h] = bits_to<T>(df_lds64(ring_base + ((ws[h] & 0xffffu) << 3)));
+            v[2 * h + 1] = bits_to<T>(df_lds64(ring_base + ((ws[h] >> 16) << 3)));
+        }
+#pragma unroll
+        for (int st = 1; st < 16; st <<= 1)
+#pragma unroll
+            for (int i = 0; i < 16; i += 2 * st) v[i] += v[i + st];
+        acc += v[0];
+    }
+    return acc;
+}
+template <typename T>
+__device__ __forceinline__ u64 df_bits(T x);
+template <>
+__device__ __forceinline__ u64 df_bits<u64>(u64 x) { return x; }
+template <>
+__device__ __forceinline__ u64 df_bits<double>(double x) { return (u64)__double_as_longlong(x); }
+
+template <typename T, int NN, int NM, int FE>
+__global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int RING = a.ring_mask + 1;
+    const int ch = 1 << a.lg_ch;
+    const unsigned ring_base = smem_u32(smem);                            // RING + 2 entries
+    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);
+    const unsigned ctrl = smem_u32(bars + ((a.nstage + 1) & ~1));         // ready, done_rank, levels_done
+    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 1) & ~1) + 16;
+    const unsigned stage_base = smem_u32(stage0);
+    const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
+    const unsigned sbytes = dbytes + gbytes + ubytes;
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
+    const int32_t nchunks = (int32_t)(a.npad >> a.lg_ch);
+
+    if (tid == 0) {
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
+        for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
+        asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
+                     : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kNWC) {
+        // ------------------------------------------------------ producer --
+        if (lane == 0) {
+            auto issue = [&](int32_t c) {
+                const int s = c & (a.nstage - 1);
+                unsigned char *st = stage0 + (size_t)s * sbytes;
+                const size_t r0 = (size_t)c << a.lg_ch;
+                mbar_expect_tx(&bars[s], sbytes);
+                bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s]);
+                bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s]);
+                bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
+            };
+            int32_t issued = 0, arrived = 0;
+            for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
+            while (arrived < nchunks) {
+                mbar_wait(&bars[arrived & (a.nstage - 1)], (unsigned)((arrived / a.nstage) & 1));
+                arrived++;
+                df_rel(ctrl, arrived << a.lg_ch);
+                while (issued < nchunks) {
+                    const int32_t done = df_acq(ctrl + 4);
+                    if (((int64_t)(issued - a.nstage + 1) << a.lg_ch) > done) {
+                        if (arrived < issued) break;
+                        __nanosleep(64);
+                        continue;
+                    }
+                    issue(issued);
+                    issued++;
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------- consumers ----
+    T *f = reinterpret_cast<T *>(a.f);
+    // level bounds of this warp's levels w, w + NWC, ...: lane i caches
+    // lvl_ptr[w + (base + i) * NWC] and the next entry
+    int32_t cb = 0;
+    auto ld_bounds = [&](int32_t i0, int32_t &vlo, int32_t &vhi) {
+        const int32_t L = warp + (i0 + lane) * kNWC;
+        vlo = a.lvl_ptr[min(L, a.ell)];
+        vhi = a.lvl_ptr[min(L + 1, a.ell)];
+    };
+    int32_t clo, chi;
+    ld_bounds(0, clo, chi);
+    int32_t staged = 0;
+    for (int32_t i = 0;; i++) {
+        const int32_t L = warp + i * kNWC;
+        if (L >= a.ell) break;
+        if (i - cb == 32) {
+            cb += 32;
+            ld_bounds(cb, clo, chi);
+        }
+        const int32_t lo = __shfl_sync(0xffffffffu, clo, i - cb);
+        const int32_t hi = __shfl_sync(0xffffffffu, chi, i - cb);
+        T fout = T(0);
+        int32_t uout = -1;
+        for (int32_t base = lo; base < hi; base += 32) {
+            if (uout >= 0) f[(size_t)uout * a.B + b] = fout;   // previous pass of a wide level
+            uout = -1;
+            const int32_t e = base + lane;
+            const bool act = e < hi;
+            const int32_t last = min(hi, base + 32);
+            while (staged < last) staged = df_acq(ctrl);
+            const unsigned st = stage_base + (unsigned)(((act ? e : base) >> a.lg_ch) & (a.nstage - 1)) * sbytes;
+            const unsigned off = (unsigned)((act ? e : base) & (ch - 1));
+            const unsigned row = st + off * (unsigned)a.kp * 2;
+            const T gx = bits_to<T>(df_lds64(st + dbytes + off * 8));
+            int32_t u;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u) : "r"(st + dbytes + gbytes + off * 4));
+            unsigned short pn16;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(pn16) : "r"(row + 2 * (NN + NM + FE)));
+            // far
+            while (df_acq(ctrl + 8) < L - kMid) {
+            }
+            T s = df_sum<T, FE>(ring_base, row + 2 * (NN + NM));
+            // mid
+            while (df_acq(ctrl + 8) < L - kNear) {
+            }
+            s += df_sum<T, NM>(ring_base, row + 2 * NN);
+            // near: the critical path
+            while (df_acq(ctrl + 8) < L) {
+            }
+            s += df_sum<T, NN>(ring_base, row);
+            const T Fprev = bits_to<T>(df_lds64(ring_base + (unsigned)pn16 * 8));
+            const T Fx = gx - s;
+            if (act)
+                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
+                             "l"(df_bits<T>(Fx))
+                             : "memory");
+            fout = Fx - Fprev;
+            uout = act ? u : -1;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // done_rank (relaxed) then levels_done (release: orders the ring
+            // stores of the whole warp, made visible to lane 0 by __syncwarp)
+            asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
+            df_rel(ctrl + 8, L + 1);
+        }
+        // the global store of f after the release: the release must not wait
+        // for it (levels wider than 32 store their earlier passes below too)
+        if (uout >= 0) f[(size_t)uout * a.B + b] = fout;
+    }
+}
+
+// ------------------------------------------------------------- host -------
+static constexpr size_t kSmemCapDF = 227 * 1024;
+
+static size_t ringdf_smem_bytes(int ring, int kp, int ch, int nstage) {
+    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
+}
+
+void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
+                 const unsigned counts2[2], RingDFPlan &R) {
+    R.ok = false;
+    if (n <= 0 || k > 256 || counts2[0] > 16 || counts2[1] > 32) return;
+    R.nn = counts2[0] <= 8 ? 8 : 16;
+    R.nm = counts2[1] <= 16 ? 16 : 32;
+    R.fe = k <= 64 ? 64 : k <= 128 ? 128 : 256;
+    int32_t kp = R.nn + R.nm + R.fe + 8;
+    if ((kp / 8) % 2 == 0) kp += 8;
+    const int64_t ahead = (int64_t)(kNWC + kMid + 4) * max_level_width;
+    int64_t ring = 32;
+    while (ring < (int64_t)reach + ahead + 1) ring <<= 1;
+    if (ring > (1 << 15)) return;
+    for (int nstage : {4, 2}) {
+        for (int ch : {256, 128, 64, 32}) {
+            if ((int64_t)(nstage - 1) * ch < (int64_t)(kNWC + 1) * max_level_width) break;
+            if (ringdf_smem_bytes((int)ring, kp, ch, nstage) <= kSmemCapDF) {
+                R.ok = true;
+                R.kp = kp;
+                R.ring = (int32_t)ring;
+                R.ch = ch;
+                R.nstage = nstage;
+                R.npad = ((int64_t)n + ch - 1) / ch * ch;
+                return;
+            }
+        }
+    }
+}
+
+cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int32_t *slot_rank,
+                             unsigned *out2, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out2, 0, 2 * sizeof(unsigned), s);
+    if (e != cudaSuccess || P.n == 0) return e;
+    k_df_counts<<<(P.n + 255) / 256, 256, 0, s>>>(P.M, P.n, P.k, P.chain, level, slot_rank, out2);
+    launches_add(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *level,
+                                const int32_t *slot_rank, cudaStream_t s) {
+    if (P.n == 0) return cudaSuccess;
+    const size_t smem = (size_t)64 * (P.k + 1) * 2 + (size_t)32 * R.kp * 2;
+    cudaError_t e = cudaFuncSetAttribute(k_build_ringdf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    k_build_ringdf<<<(unsigned)(R.npad / 32), 256, smem, s>>>(P.M, P.n, P.k, R.kp, R.nn, R.nm, R.fe,
+                                                              R.ring, P.chain, P.slot, slot_rank,
+                                                              level, R.D);
+    launches_add(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
+                                  int dtype, const void *gP, void *f, int64_t B, cudaStream_t s) {
+    if (P.n == 0) return cudaSuccess;
+    RDFArgs a;
+    a.D = R.D;
+    a.gP = gP;
+    a.ru = ru_pad;
+    a.lvl_ptr = P.lvl_ptr;
+    a.f = f;
+    a.npad = R.npad;
+    a.n = P.n;
+    a.kp = R.kp;
+    a.ell = P.ell;
+    a.B = (int32_t)B;
+    a.ring_mask = R.ring - 1;
+    a.lg_ch = 0;
+    while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
+    a.nstage = R.nstage;
+    const size_t smem = ringdf_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
+    void *fn = nullptr;
+#define RDF_FN(NN, NM, FE)                                                                     \
+    if (R.nn == NN && R.nm == NM && R.fe == FE)                                                \
+        fn = dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE> : (void *)k_moeb_ringdf<double, NN, NM, FE>;
+    RDF_FN(8, 16, 64) RDF_FN(8, 32, 64) RDF_FN(16, 16, 64) RDF_FN(16, 32, 64)
+    RDF_FN(8, 16, 128) RDF_FN(8, 32, 128) RDF_FN(16, 16, 128) RDF_FN(16, 32, 128)
+    RDF_FN(8, 16, 256) RDF_FN(8, 32, 256) RDF_FN(16, 16, 256) RDF_FN(16, 32, 256)
+#undef RDF_FN
+    if (!fn) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void *args[] = {&a};
+    launches_add(1);
+    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNWC + 1)), args, smem, s);
+}
+
+}  // namespace poset

@@ -28,8 +28,8 @@ for lpe in (1, 2, 4, 8):
     ms = prof["moebius_solve"][0] / 3
     res[f"lpe{lpe}_ms"] = ms
     res[f"lpe{lpe}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
-for kern, name in ((pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
-    if kern == pz.MOEB_RINGWS and not info["ringws"]:
+for kern, name in ((pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
+    if (kern == pz.MOEB_RINGWS and not info["ringws"]) or (kern == pz.MOEB_RINGDF and not info["ringdf"]):
         continue
     P.set_option("ring_lpe", 8)
     P.set_option("moebius_kernel", kern)
