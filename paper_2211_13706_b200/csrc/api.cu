@@ -651,10 +651,18 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         }
         return POSET_OK;
     }
-    if (!strcmp(key, "ring_debug")) {   // timing experiments only (bit 0: results NOT valid)
-        h->ring.debug = (int32_t)value;
+    if (!strcmp(key, "ringdf_nwc")) {   // RINGDF consumer warps (tuning)
+        if (!h->rdf.ok || (value != 4 && value != 8)) return fail(POSET_EINVAL, "ringdf_nwc is 4 or 8");
+        h->rdf.nwc = (int32_t)value;
+        return POSET_OK;
+    }
+    if (!strcmp(key, "ring_debug")) {   // timing experiments only (bit 0: results NOT valid,
+                                         // bit 3: instrumented RINGDF -> poset_debug_read)
+        h->ring.debug = (int32_t)(value & 1);
         if (!h->ring.dbg) CK(cudaMalloc((void **)&h->ring.dbg, 64));
         CK(cudaMemset(h->ring.dbg, 0, 64));
+        h->rdf.prof = (value & 8) != 0;
+        h->rdf.dbg = h->ring.dbg;
         return POSET_OK;
     }
     if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)

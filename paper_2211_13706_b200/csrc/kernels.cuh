@@ -131,6 +131,9 @@ struct RingDFPlan {
     bool ok = false;
     int32_t nn = 0, nm = 0, fe = 0;   // near / mid / far row entries
     int32_t kp = 0, ring = 0, ch = 0, nstage = 0;
+    int32_t nwc = 8;                  // consumer warps (4 or 8)
+    bool prof = false;                // instrumented instantiation (tuning)
+    unsigned long long *dbg = nullptr;
     int64_t npad = 0;
     uint16_t *D = nullptr;
 };

@@ -38,7 +38,6 @@ typedef unsigned long long u64;
 
 static constexpr int kNear = 2;    // level distance <= kNear: near
 static constexpr int kMid = 6;     // kNear < distance <= kMid: mid; beyond: far
-static constexpr int kNWC = 8;     // consumer warps per CTA
 
 // ------------------------------------------------------------ setup -------
 // max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
@@ -146,6 +145,8 @@ struct RDFArgs {
     int32_t n, kp, ell, B;
     int32_t ring_mask;
     int32_t lg_ch, nstage;
+    unsigned long long *dbg;    // PROF instantiation only: [0] Σ ready->publish, [1] Σ publish->ready
+                                // (owner already waiting), [2] Σ lateness, [3] late levels, [4] levels
 };
 
 __device__ __forceinline__ uint4 df_lds128(unsigned addr) {
@@ -201,6 +202,25 @@ __device__ __forceinline__ T df_sum(unsigned ring_base, unsigned row) {
     }
     return acc;
 }
+// Σ ring[slot] for E slots already in registers (two per 32-bit word)
+template <typename T, int E>
+__device__ __forceinline__ T df_sum_w(unsigned ring_base, const uint4 (&w)[E / 8]) {
+    T v[E];
+#pragma unroll
+    for (int i = 0; i < E / 8; i++) {
+        const unsigned ws[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            v[8 * i + 2 * h] = bits_to<T>(df_lds64(ring_base + ((ws[h] & 0xffffu) << 3)));
+            v[8 * i + 2 * h + 1] = bits_to<T>(df_lds64(ring_base + ((ws[h] >> 16) << 3)));
+        }
+    }
+#pragma unroll
+    for (int st = 1; st < E; st <<= 1)
+#pragma unroll
+        for (int i = 0; i < E; i += 2 * st) v[i] += v[i + st];
+    return v[0];
+}
 template <typename T>
 __device__ __forceinline__ u64 df_bits(T x);
 template <>
@@ -208,7 +228,7 @@ __device__ __forceinline__ u64 df_bits<u64>(u64 x) { return x; }
 template <>
 __device__ __forceinline__ u64 df_bits<double>(double x) { return (u64)__double_as_longlong(x); }
 
-template <typename T, int NN, int NM, int FE>
+template <typename T, int NN, int NM, int FE, int kNWC, bool PROF = false>
 __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
@@ -233,12 +253,13 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    const unsigned ns = (unsigned)a.nstage;   // any stage count 2..8 (not only powers of two)
 
     if (warp == kNWC) {
         // ------------------------------------------------------ producer --
         if (lane == 0) {
             auto issue = [&](int32_t c) {
-                const int s = c & (a.nstage - 1);
+                const int s = (int)((unsigned)c % ns);
                 unsigned char *st = stage0 + (size_t)s * sbytes;
                 const size_t r0 = (size_t)c << a.lg_ch;
                 mbar_expect_tx(&bars[s], sbytes);
@@ -249,7 +270,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             int32_t issued = 0, arrived = 0;
             for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
             while (arrived < nchunks) {
-                mbar_wait(&bars[arrived & (a.nstage - 1)], (unsigned)((arrived / a.nstage) & 1));
+                mbar_wait(&bars[(unsigned)arrived % ns], ((unsigned)arrived / ns) & 1u);
                 arrived++;
                 df_rel(ctrl, arrived << a.lg_ch);
                 while (issued < nchunks) {
@@ -269,6 +290,12 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
 
     // ------------------------------------------------------- consumers ----
     T *f = reinterpret_cast<T *>(a.f);
+    // PROF: per-CTA counters in the (otherwise unused) zero-padding of the ring
+    __shared__ unsigned long long prof[5];
+    __shared__ volatile unsigned long long prof_last;
+    long long t_ready = 0;
+    if (PROF && tid == 0) { for (int i = 0; i < 5; i++) prof[i] = 0; prof_last = clock64(); }
+    if (PROF) asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
     // level bounds of this warp's levels w, w + NWC, ...: lane i caches
     // lvl_ptr[w + (base + i) * NWC] and the next entry
     int32_t cb = 0;
@@ -298,7 +325,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             const bool act = e < hi;
             const int32_t last = min(hi, base + 32);
             while (staged < last) staged = df_acq(ctrl);
-            const unsigned st = stage_base + (unsigned)(((act ? e : base) >> a.lg_ch) & (a.nstage - 1)) * sbytes;
+            const unsigned st = stage_base + ((unsigned)((act ? e : base) >> a.lg_ch) % ns) * sbytes;
             const unsigned off = (unsigned)((act ? e : base) & (ch - 1));
             const unsigned row = st + off * (unsigned)a.kp * 2;
             const T gx = bits_to<T>(df_lds64(st + dbytes + off * 8));
@@ -314,10 +341,23 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             while (df_acq(ctrl + 8) < L - kNear) {
             }
             s += df_sum<T, NM>(ring_base, row + 2 * NN);
-            // near: the critical path
+            // near: the critical path (row words loaded before the wait)
+            uint4 nw[NN / 8];
+#pragma unroll
+            for (int i = 0; i < NN / 8; i++) nw[i] = df_lds128(row + 16 * i);
+            long long t_wait = 0;
+            if (PROF) t_wait = clock64();
             while (df_acq(ctrl + 8) < L) {
             }
-            s += df_sum<T, NN>(ring_base, row);
+            if (PROF && base == lo) {
+                t_ready = clock64();
+                if (lane == 0 && b == 0 && L > 0) {
+                    const long long tp = (long long)prof_last;
+                    if (t_wait > tp) { prof[2] += t_wait - tp; prof[3] += 1; }
+                    else prof[1] += t_ready - tp;
+                }
+            }
+            s += df_sum_w<T, NN>(ring_base, nw);
             const T Fprev = bits_to<T>(df_lds64(ring_base + (unsigned)pn16 * 8));
             const T Fx = gx - s;
             if (act)
@@ -333,10 +373,21 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             // stores of the whole warp, made visible to lane 0 by __syncwarp)
             asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
             df_rel(ctrl + 8, L + 1);
+            if (PROF && b == 0) {
+                const long long t = clock64();
+                prof[0] += t - t_ready;
+                prof[4] += 1;
+                prof_last = (unsigned long long)t;
+            }
         }
         // the global store of f after the release: the release must not wait
         // for it (levels wider than 32 store their earlier passes below too)
         if (uout >= 0) f[(size_t)uout * a.B + b] = fout;
+    }
+    if (PROF) {
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
+        if (tid == 0 && b == 0)
+            for (int i = 0; i < 5; i++) a.dbg[i] = prof[i];
     }
 }
 
@@ -356,20 +407,23 @@ void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
     R.fe = k <= 64 ? 64 : k <= 128 ? 128 : 256;
     int32_t kp = R.nn + R.nm + R.fe + 8;
     if ((kp / 8) % 2 == 0) kp += 8;
-    const int64_t ahead = (int64_t)(kNWC + kMid + 4) * max_level_width;
+    const int64_t ahead = (int64_t)(8 + kMid + 4) * max_level_width;   // up to 8 consumer warps
     int64_t ring = 32;
     while (ring < (int64_t)reach + ahead + 1) ring <<= 1;
     if (ring > (1 << 15)) return;
-    for (int nstage : {4, 2}) {
-        for (int ch : {256, 128, 64, 32}) {
-            if ((int64_t)(nstage - 1) * ch < (int64_t)(kNWC + 1) * max_level_width) break;
-            if (ringdf_smem_bytes((int)ring, kp, ch, nstage) <= kSmemCapDF) {
+    // the fewest stages of the largest chunk that hold 9 levels and fit
+    for (int ch : {256, 128, 64, 32}) {
+        for (int nstage = 2; nstage <= 8; nstage++) {
+            if ((int64_t)(nstage - 1) * ch < (int64_t)(8 + 1) * max_level_width) continue;
+            if (ringdf_smem_bytes((int)ring, kp, ch, nstage) > kSmemCapDF) break;
+            {
                 R.ok = true;
                 R.kp = kp;
                 R.ring = (int32_t)ring;
                 R.ch = ch;
                 R.nstage = nstage;
                 R.npad = ((int64_t)n + ch - 1) / ch * ch;
+                R.nwc = 8;
                 return;
             }
         }
@@ -417,21 +471,27 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
     a.lg_ch = 0;
     while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
     a.nstage = R.nstage;
+    a.dbg = R.dbg;
     const size_t smem = ringdf_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
     void *fn = nullptr;
-#define RDF_FN(NN, NM, FE)                                                                     \
-    if (R.nn == NN && R.nm == NM && R.fe == FE)                                                \
-        fn = dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE> : (void *)k_moeb_ringdf<double, NN, NM, FE>;
-    RDF_FN(8, 16, 64) RDF_FN(8, 32, 64) RDF_FN(16, 16, 64) RDF_FN(16, 32, 64)
-    RDF_FN(8, 16, 128) RDF_FN(8, 32, 128) RDF_FN(16, 16, 128) RDF_FN(16, 32, 128)
-    RDF_FN(8, 16, 256) RDF_FN(8, 32, 256) RDF_FN(16, 16, 256) RDF_FN(16, 32, 256)
+#define RDF_FN(NN, NM, FE, W)                                                                  \
+    if (R.nn == NN && R.nm == NM && R.fe == FE && R.nwc == W)                                  \
+        fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE, W, true>            \
+                                  : (void *)k_moeb_ringdf<double, NN, NM, FE, W, true>)        \
+                    : (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE, W>                  \
+                                  : (void *)k_moeb_ringdf<double, NN, NM, FE, W>);
+#define RDF_W(NN, NM, FE) RDF_FN(NN, NM, FE, 4) RDF_FN(NN, NM, FE, 8)
+    RDF_W(8, 16, 64) RDF_W(8, 32, 64) RDF_W(16, 16, 64) RDF_W(16, 32, 64)
+    RDF_W(8, 16, 128) RDF_W(8, 32, 128) RDF_W(16, 16, 128) RDF_W(16, 32, 128)
+    RDF_W(8, 16, 256) RDF_W(8, 32, 256) RDF_W(16, 16, 256) RDF_W(16, 32, 256)
+#undef RDF_W
 #undef RDF_FN
     if (!fn) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     void *args[] = {&a};
     launches_add(1);
-    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNWC + 1)), args, smem, s);
+    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (R.nwc + 1)), args, smem, s);
 }
 
 }  // namespace poset

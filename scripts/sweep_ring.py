@@ -77,6 +77,24 @@ for _ in range(3):
     P.moebius(gi, out=yi)
 prof, _ = P.profile_read(); P.set_option("profile", 0)
 res["ring8_i64_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
+if info["ringdf"]:
+    P.set_option("moebius_kernel", pz.MOEB_RINGDF)
+    for nwc in (4, 8):
+        P.set_option("ringdf_nwc", nwc)
+        P.moebius(g, out=y); torch.cuda.synchronize()
+        P.set_option("profile", 1); P.profile_read()
+        for _ in range(3):
+            P.moebius(g, out=y)
+        prof, _ = P.profile_read(); P.set_option("profile", 0)
+        res[f"ringdf_nwc{nwc}_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
+    P.set_option("ringdf_nwc", 8)
+    P.set_option("ring_debug", 8)
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    d = P.debug_read()
+    lv = max(1, int(d[4]))
+    res["ringdf_prof"] = {"ready_to_publish": d[0] / lv, "publish_to_ready_when_waiting": d[1] / max(1, lv - d[3]),
+                          "late_levels_frac": d[3] / lv, "lateness_when_late": d[2] / max(1, d[3]), "levels": lv}
+    P.set_option("ring_debug", 0)
 res["ok_roundtrip_i64"] = None
 xi = torch.from_numpy(W.int_values(wl.n, 4, -1000, 1000, seed=3)).cuda()
 gi = P.zeta(xi)
