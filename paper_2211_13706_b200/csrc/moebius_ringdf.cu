@@ -6,9 +6,10 @@
 // P:L709-733; Alg. 5 P:L692-705 puts a barrier between levels).
 //
 // Here there is no barrier.  One CTA per column; consumer warp w owns the
-// levels L ≡ w (mod NWC), one lane per element.  A single shared counter
-// `levels_done` (levels < levels_done are finished; it advances in level
-// order) replaces the barrier.  The dependencies of an element of level L are
+// levels L ≡ w (mod NWC), one lane per element.  Level completion is
+// published on a small ring of mbarriers (arrive.release by the owner warp's
+// lanes, try_wait.parity by later owners; levels finish in order) instead of
+// a CTA barrier.  The dependencies of an element of level L are
 // split by their own level when the tables are built:
 //   far   level <= L - 7   summed once levels_done >= L - 6
 //   mid   level in [L-6, L-3]   summed once levels_done >= L - 2
@@ -38,6 +39,8 @@ typedef unsigned long long u64;
 
 static constexpr int kNear = 2;    // level distance <= kNear: near
 static constexpr int kMid = 6;     // kNear < distance <= kMid: mid; beyond: far
+static constexpr int kLB = 16;     // level-completion mbarriers (ring), > kMid + 1
+static constexpr int kNP = 3;      // passes of 32 elements kept in registers per level
 
 // ------------------------------------------------------------ setup -------
 // max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
@@ -235,8 +238,8 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     const int ch = 1 << a.lg_ch;
     const unsigned ring_base = smem_u32(smem);                            // RING + 2 entries
     u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);
-    const unsigned ctrl = smem_u32(bars + ((a.nstage + 1) & ~1));         // ready, done_rank, levels_done
-    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 1) & ~1) + 16;
+    const unsigned ctrl = smem_u32(bars + ((a.nstage + kLB + 1) & ~1));   // ready, done_rank
+    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + kLB + 1) & ~1) + 16;
     const unsigned stage_base = smem_u32(stage0);
     const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
     const unsigned sbytes = dbytes + gbytes + ubytes;
@@ -248,6 +251,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     if (tid == 0) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
         for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 32);
         asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
                      : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -289,15 +293,23 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     }
 
     // ------------------------------------------------------- consumers ----
+    // Level completion is published on a ring of kLB mbarriers: the 32 lanes
+    // of the warp that owns level L arrive (release) on lvlbar[L % kLB] once
+    // their ring stores are issued; a waiter for "level L done" try_waits
+    // (acquire) on the phase (L / kLB) & 1.  Levels finish in order, so "L
+    // done" means every level <= L is done, and no waiter ever looks more
+    // than kMid + 1 < kLB levels back, so parities cannot alias.
     T *f = reinterpret_cast<T *>(a.f);
-    // PROF: per-CTA counters in the (otherwise unused) zero-padding of the ring
+    u64 *lvlbar = bars + a.nstage;   // kLB barriers after the stage barriers
     __shared__ unsigned long long prof[5];
     __shared__ volatile unsigned long long prof_last;
     long long t_ready = 0;
     if (PROF && tid == 0) { for (int i = 0; i < 5; i++) prof[i] = 0; prof_last = clock64(); }
     if (PROF) asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
-    // level bounds of this warp's levels w, w + NWC, ...: lane i caches
-    // lvl_ptr[w + (base + i) * NWC] and the next entry
+    auto wait_level = [&](int32_t Ld) {   // level Ld (and all below) done
+        if (Ld < 0) return;
+        mbar_wait(&lvlbar[Ld & (kLB - 1)], (unsigned)((Ld / kLB) & 1));
+    };
     int32_t cb = 0;
     auto ld_bounds = [&](int32_t i0, int32_t &vlo, int32_t &vhi) {
         const int32_t L = warp + (i0 + lane) * kNWC;
@@ -316,63 +328,89 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         }
         const int32_t lo = __shfl_sync(0xffffffffu, clo, i - cb);
         const int32_t hi = __shfl_sync(0xffffffffu, chi, i - cb);
-        T fout = T(0);
-        int32_t uout = -1;
-        for (int32_t base = lo; base < hi; base += 32) {
-            if (uout >= 0) f[(size_t)uout * a.B + b] = fout;   // previous pass of a wide level
-            uout = -1;
-            const int32_t e = base + lane;
-            const bool act = e < hi;
-            const int32_t last = min(hi, base + 32);
-            while (staged < last) staged = df_acq(ctrl);
-            const unsigned st = stage_base + ((unsigned)((act ? e : base) >> a.lg_ch) % ns) * sbytes;
-            const unsigned off = (unsigned)((act ? e : base) & (ch - 1));
-            const unsigned row = st + off * (unsigned)a.kp * 2;
-            const T gx = bits_to<T>(df_lds64(st + dbytes + off * 8));
-            int32_t u;
-            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u) : "r"(st + dbytes + gbytes + off * 4));
-            unsigned short pn16;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(pn16) : "r"(row + 2 * (NN + NM + FE)));
-            // far
-            while (df_acq(ctrl + 8) < L - kMid) {
-            }
-            T s = df_sum<T, FE>(ring_base, row + 2 * (NN + NM));
-            // mid
-            while (df_acq(ctrl + 8) < L - kNear) {
-            }
-            s += df_sum<T, NM>(ring_base, row + 2 * NN);
-            // near: the critical path (row words loaded before the wait)
-            uint4 nw[NN / 8];
+        const int32_t npass = (hi - lo + 31) >> 5;
+        const int32_t np = min(npass, kNP);
+        while (staged < hi) staged = df_acq(ctrl);
+        // per pass: row-derived data in registers (passes beyond kNP: serial below)
+        T gx[kNP], sp[kNP];
+        int32_t u[kNP];
+        unsigned rowa[kNP], pn[kNP];
+        uint4 nw[kNP][NN / 8];
 #pragma unroll
-            for (int i = 0; i < NN / 8; i++) nw[i] = df_lds128(row + 16 * i);
-            long long t_wait = 0;
-            if (PROF) t_wait = clock64();
-            while (df_acq(ctrl + 8) < L) {
+        for (int p = 0; p < kNP; p++) {
+            if (p < np) {
+                const int32_t e = lo + 32 * p + lane;
+                const int32_t ee = e < hi ? e : lo + 32 * p;
+                const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
+                const unsigned off = (unsigned)(ee & (ch - 1));
+                rowa[p] = st + off * (unsigned)a.kp * 2;
+                gx[p] = bits_to<T>(df_lds64(st + dbytes + off * 8));
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + dbytes + gbytes + off * 4));
+                unsigned short pn16;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=h"(pn16) : "r"(rowa[p] + 2 * (NN + NM + FE)));
+                pn[p] = pn16;
+#pragma unroll
+                for (int q = 0; q < NN / 8; q++) nw[p][q] = df_lds128(rowa[p] + 16 * q);
+                u[p] = e < hi ? u[p] : -1;
             }
-            if (PROF && base == lo) {
-                t_ready = clock64();
-                if (lane == 0 && b == 0 && L > 0) {
-                    const long long tp = (long long)prof_last;
-                    if (t_wait > tp) { prof[2] += t_wait - tp; prof[3] += 1; }
-                    else prof[1] += t_ready - tp;
-                }
+        }
+        wait_level(L - kMid - 1);   // far: levels <= L-7
+#pragma unroll
+        for (int p = 0; p < kNP; p++)
+            if (p < np) sp[p] = df_sum<T, FE>(ring_base, rowa[p] + 2 * (NN + NM));
+        wait_level(L - kNear - 1);  // mid: levels <= L-3
+#pragma unroll
+        for (int p = 0; p < kNP; p++)
+            if (p < np) sp[p] += df_sum<T, NM>(ring_base, rowa[p] + 2 * NN);
+        long long t_wait = 0;
+        if (PROF) t_wait = clock64();
+        wait_level(L - 1);          // near: the critical path
+        if (PROF) {
+            t_ready = clock64();
+            if (lane == 0 && b == 0 && L > 0) {
+                const long long tp = (long long)prof_last;
+                if (t_wait > tp) { prof[2] += t_wait - tp; prof[3] += 1; }
+                else prof[1] += t_ready - tp;
             }
-            s += df_sum_w<T, NN>(ring_base, nw);
-            const T Fprev = bits_to<T>(df_lds64(ring_base + (unsigned)pn16 * 8));
-            const T Fx = gx - s;
-            if (act)
+        }
+        T fo[kNP];
+#pragma unroll
+        for (int p = 0; p < kNP; p++) {
+            if (p < np) {
+                const T Fx = gx[p] - (sp[p] + df_sum_w<T, NN>(ring_base, nw[p]));
+                fo[p] = Fx - bits_to<T>(df_lds64(ring_base + pn[p] * 8));
+                if (u[p] >= 0)
+                    asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8),
+                                 "l"(df_bits<T>(Fx))
+                                 : "memory");
+            }
+        }
+        // passes beyond kNP (levels wider than 32 * kNP): serially, all deps done
+        for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
+            const int32_t e = base + lane;
+            const int32_t ee = e < hi ? e : base;
+            const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
+            const unsigned off = (unsigned)(ee & (ch - 1));
+            const unsigned row = st + off * (unsigned)a.kp * 2;
+            const T g1 = bits_to<T>(df_lds64(st + dbytes + off * 8));
+            int32_t u1;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + dbytes + gbytes + off * 4));
+            unsigned short p16;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(p16) : "r"(row + 2 * (NN + NM + FE)));
+            const T Fx = g1 - (df_sum<T, FE>(ring_base, row + 2 * (NN + NM)) + df_sum<T, NM>(ring_base, row + 2 * NN) +
+                               df_sum<T, NN>(ring_base, row));
+            if (e < hi) {
                 asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
                              "l"(df_bits<T>(Fx))
                              : "memory");
-            fout = Fx - Fprev;
-            uout = act ? u : -1;
+                f[(size_t)u1 * a.B + b] = Fx - bits_to<T>(df_lds64(ring_base + (unsigned)p16 * 8));
+            }
         }
-        __syncwarp();
+        // publish: every lane releases its own ring stores
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
+                     : "memory");
         if (lane == 0) {
-            // done_rank (relaxed) then levels_done (release: orders the ring
-            // stores of the whole warp, made visible to lane 0 by __syncwarp)
             asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
-            df_rel(ctrl + 8, L + 1);
             if (PROF && b == 0) {
                 const long long t = clock64();
                 prof[0] += t - t_ready;
@@ -380,9 +418,9 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 prof_last = (unsigned long long)t;
             }
         }
-        // the global store of f after the release: the release must not wait
-        // for it (levels wider than 32 store their earlier passes below too)
-        if (uout >= 0) f[(size_t)uout * a.B + b] = fout;
+#pragma unroll
+        for (int p = 0; p < kNP; p++)
+            if (p < np && u[p] >= 0) f[(size_t)u[p] * a.B + b] = fo[p];
     }
     if (PROF) {
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
@@ -395,7 +433,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
 static constexpr size_t kSmemCapDF = 227 * 1024;
 
 static size_t ringdf_smem_bytes(int ring, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
+    return (size_t)(ring + 2) * 8 + 8 * ((nstage + kLB + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
 }
 
 void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
