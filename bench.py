@@ -38,7 +38,7 @@ PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
                 "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
                 "chain_diff": "k_chain_diff"}
-MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf"]
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf", "ringfr"]
 
 
 def parse():
@@ -143,7 +143,7 @@ def alg_bytes(n, k, B, info=None):
         d["gather"] = sparse + 16 * n * B + 4 * n
     if info is not None and info.get("moebius_kernel") == 5:
         d["moebius_solve"] = info["csr_bytes"] + 32 * n * B + 8 * n   # rows, g, F w+r, f
-    if info is not None and info.get("moebius_kernel") in (4, 6, 7):
+    if info is not None and info.get("moebius_kernel") in (4, 6, 7, 8):
         # RING: distance table once (shared by the B CTAs through L2), gP read,
         # f written, rank->user rows; F never leaves shared memory
         d["moebius_solve"] = info["dist_bytes"] + 16 * n * B + 4 * n

@@ -78,9 +78,13 @@ typedef enum {
     POSET_MOEB_RINGWS = 6,    /* RING with warp specialisation: one warp on the level-by-level
                                  critical path (near dependencies only), the others summing the
                                  far dependencies ahead of it                 */
-    POSET_MOEB_RINGDF = 7     /* barrier-free level pipeline: warps own levels round-robin and
-                                 sync through one levels-done counter; far / mid dependencies
-                                 are summed levels ahead, near ones on the critical path     */
+    POSET_MOEB_RINGDF = 7,    /* barrier-free level pipeline: warps own levels round-robin and
+                                 publish level completion through mbarriers; far / mid
+                                 dependencies are summed levels ahead, near ones on the
+                                 critical path                                               */
+    POSET_MOEB_RINGFR = 8     /* experimental (slower than RINGDF on C5w, never chosen by AUTO):
+                                 RINGDF tables, critical path kept in one "fresh" warp,
+                                 far + mid sums by helper warps             */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -107,7 +111,7 @@ typedef struct {
     int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
     int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
-    int64_t ringdf;       /* 1 if the RINGDF schedule is available                  */
+    int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGFR available       */
 } poset_info;
 
 /*

@@ -232,7 +232,7 @@ static poset_status finish_setup(poset_s *h) {
                    (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0) +
                    (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
-    I.ringdf = h->rdf.ok ? 1 : 0;
+    I.ringdf = h->rdf.ok ? (h->rdf.fr_ok ? 3 : 1) : 0;   // bit 1: RINGFR available
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
@@ -414,6 +414,19 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
+    if (which == MOEB_RINGFR) {
+        if (!h->rdf.ok || !h->rdf.fr_ok)
+            return fail(POSET_EINVAL, "poset_moebius: the RINGFR schedule does not fit this poset; use AUTO");
+        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
+        if (st) return st;
+        {
+            PhaseTimer t(h, POSET_PH_PERM, s);
+            CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
+        }
+        PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        CK(launch_moebius_ringfr(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+        return POSET_OK;
+    }
     if (which == MOEB_RINGDF) {
         if (!h->rdf.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
@@ -626,7 +639,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_RINGDF) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RINGFR) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }
@@ -662,6 +675,7 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         if (!h->ring.dbg) CK(cudaMalloc((void **)&h->ring.dbg, 64));
         CK(cudaMemset(h->ring.dbg, 0, 64));
         h->rdf.prof = (value & 8) != 0;
+        h->rdf.skip_far = (int32_t)((value >> 4) & 7);   // bits 4-6: RINGDF without far / mid / near sums
         h->rdf.dbg = h->ring.dbg;
         return POSET_OK;
     }

@@ -28,8 +28,9 @@ for lpe in (1, 2, 4, 8):
     ms = prof["moebius_solve"][0] / 3
     res[f"lpe{lpe}_ms"] = ms
     res[f"lpe{lpe}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
-for kern, name in ((pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
-    if (kern == pz.MOEB_RINGWS and not info["ringws"]) or (kern == pz.MOEB_RINGDF and not info["ringdf"]):
+for kern, name in ((pz.MOEB_RINGFR, "ringfr"), (pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
+    if (kern == pz.MOEB_RINGWS and not info["ringws"]) or (kern == pz.MOEB_RINGDF and not info["ringdf"] & 1) \
+            or (kern == pz.MOEB_RINGFR and not info["ringdf"] & 2):
         continue
     P.set_option("ring_lpe", 8)
     P.set_option("moebius_kernel", kern)
@@ -93,7 +94,16 @@ if info["ringdf"]:
     d = P.debug_read()
     lv = max(1, int(d[4]))
     res["ringdf_prof"] = {"ready_to_publish": d[0] / lv, "publish_to_ready_when_waiting": d[1] / max(1, lv - d[3]),
-                          "late_levels_frac": d[3] / lv, "lateness_when_late": d[2] / max(1, d[3]), "levels": lv}
+                          "late_levels_frac": d[3] / lv, "lateness_when_late": d[2] / max(1, d[3]), "levels": lv,
+                          "ready_to_before_arrive": d[5] / lv, "avg_passes": d[6] / lv, "ready_to_near_sum": d[7] / lv}
+    for bits, name in ((16, "nofar"), (48, "nofar_nomid"), (112, "nofar_nomid_nonear")):
+        P.set_option("ring_debug", bits)
+        P.moebius(g, out=y); torch.cuda.synchronize()
+        P.set_option("profile", 1); P.profile_read()
+        for _ in range(3):
+            P.moebius(g, out=y)
+        prof, _ = P.profile_read(); P.set_option("profile", 0)
+        res[f"ringdf_{name}_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
     P.set_option("ring_debug", 0)
 res["ok_roundtrip_i64"] = None
 xi = torch.from_numpy(W.int_values(wl.n, 4, -1000, 1000, seed=3)).cuda()
