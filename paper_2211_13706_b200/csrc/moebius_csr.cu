@@ -113,7 +113,7 @@ template <typename T, bool CG>
 __device__ __forceinline__ T row_sum_lanes(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                            const T *Fsrc, int32_t B, int c) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = 8;
+    constexpr int U = 16;
     T s[U];
 #pragma unroll
     for (int u = 0; u < U; u++) s[u] = T(0);
@@ -146,7 +146,7 @@ template <typename T, bool CG>
 __device__ __forceinline__ T row_sum_cols(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                           const T *Fsrc, int32_t B, int col) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = 16;
+    constexpr int U = 32;
     T s[U];
 #pragma unroll
     for (int u = 0; u < U; u++) s[u] = T(0);
@@ -228,20 +228,18 @@ cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, co
 }
 
 // ------------------------------------------------------ Möbius (CSR) ------
-__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks) {
+// Grid barrier on a monotone arrival counter: barrier number t completes when
+// the counter reaches (t + 1) * nblocks.  One release-add per CTA and an
+// acquire spin by one thread; no reset, no generation flag.
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks, unsigned t) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g0) __nanosleep(20);
-        }
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned target = (t + 1) * nblocks;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while ((int)(v - target) < 0);
     }
     __syncthreads();
 }
@@ -280,7 +278,7 @@ __global__ void __launch_bounds__(512) k_moeb_csr(DevPoset P, const int64_t *__r
                 }
             }
         }
-        if (L + 1 < P.ell) grid_sync(bar, gridDim.x);
+        if (L + 1 < P.ell) grid_sync(bar, gridDim.x, (unsigned)L);
     }
 }
 
