@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
 // publishes level completion on lvl_bar[L % kLB] (arrive.release by its 32
 // lanes) for the helpers; it normally finds sold_bar[L] already complete.
 template <typename T, int NN, int NM, int FE, int kNH>
-__global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
+__global__ void __launch_bounds__(32 * (kNH + 3)) k_moeb_ringfr(RDFArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
     const int ch = 1 << a.lg_ch;
@@ -504,7 +504,11 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
     T *sold = reinterpret_cast<T *>(smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 2 * kLB + 1) & ~1) + 16);
     const int SB = a.sbuf;   // S_old entries (power of two), indexed by rank
     int *stag = reinterpret_cast<int *>(sold + SB);   // rank whose S_old is in the slot
-    unsigned char *stage0 = reinterpret_cast<unsigned char *>(stag + SB);
+    // f output buffer (fresh warp -> writer warp): value and user id per rank
+    constexpr int FB = 1024;
+    T *fbuf = reinterpret_cast<T *>(stag + SB);
+    int *fusr = reinterpret_cast<int *>(fbuf + FB);
+    unsigned char *stage0 = reinterpret_cast<unsigned char *>(fusr + FB);
     const unsigned stage_base = smem_u32(stage0);
     const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
     const unsigned sbytes = dbytes + gbytes + ubytes;
@@ -519,7 +523,8 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
         for (int s2 = 0; s2 < a.nstage; s2++) mbar_init(&bars[s2], 1);
         for (int s2 = 0; s2 < 2 * kLB; s2++) mbar_init(&lvlbar[s2], 32);
-        asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;" ::"r"(ctrl) : "memory");
+        asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
+                     : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -561,6 +566,26 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
                     issued++;
                 }
             }
+        }
+        return;
+    }
+
+    if (warp == kNH + 2) {
+        // -------------------------------------------------------- writer --
+        // drains fbuf: ranks < done_rank (published with release by the
+        // fresh warp) are final; publishes drained (ctrl + 8) for slot reuse
+        T *f = reinterpret_cast<T *>(a.f);
+        int32_t w = 0;
+        while (w < a.n) {
+            const int32_t done = df_acq(ctrl + 4);
+            if (done <= w) { __nanosleep(32); continue; }
+            for (int32_t r = w + lane; r < done; r += 32) {
+                const int i = r & (FB - 1);
+                f[(size_t)fusr[i] * a.B + b] = fbuf[i];
+            }
+            __syncwarp();
+            w = done;
+            if (lane == 0) df_rel(ctrl + 8, w);
         }
         return;
     }
@@ -656,6 +681,7 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
         R.so = sold[ee & (SB - 1)];
     };
     int32_t lo, hi;
+    int32_t drained = 0;
     bounds(0, lo, hi);
     Row R;
     while (staged < hi) staged = df_acq(ctrl);
@@ -675,10 +701,12 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
         {
             const T Fx = R.g - (R.so + sn);
             if (R.u >= 0) {
-                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)((lo + lane) & a.ring_mask) * 8),
+                const int e = lo + lane;
+                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
                              "l"(df_bits<T>(Fx))
                              : "memory");
-                f[(size_t)R.u * a.B + b] = Fx - Fp;
+                fbuf[e & (FB - 1)] = Fx - Fp;
+                fusr[e & (FB - 1)] = R.u;
             }
         }
         for (int32_t base = lo + 32; base < hi; base += 32) {   // further passes of a wide level
@@ -687,17 +715,24 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
             const T Fx = Rx.g - (Rx.so + df_sum_wc<T, NN>(ring_base, Rx.nw, (int)(Rx.pc >> 16) & 0xff));
             const T Fq = bits_to<T>(df_lds64(ring_base + (Rx.pc & 0xffffu)));
             if (Rx.u >= 0) {
-                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)((base + lane) & a.ring_mask) * 8),
+                const int e = base + lane;
+                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
                              "l"(df_bits<T>(Fx))
                              : "memory");
-                f[(size_t)Rx.u * a.B + b] = Fx - Fq;
+                fbuf[e & (FB - 1)] = Fx - Fq;
+                fusr[e & (FB - 1)] = Rx.u;
             }
         }
         __syncwarp();
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
                      : "memory");
-        if (lane == 0) asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
+        if (lane == 0) df_rel(ctrl + 4, hi);   // ranks < hi final (producer, writer)
         R = Rn;
+        // fbuf slots of the next level must have been drained
+        if (nhi - FB > drained) {
+            while ((drained = df_acq(ctrl + 8)) < nhi - FB) {
+            }
+        }
         lo = nlo;
         hi = nhi;
     }
@@ -707,7 +742,7 @@ __global__ void __launch_bounds__(32 * (kNH + 2)) k_moeb_ringfr(RDFArgs a) {
 static constexpr size_t kSmemCapDF = 227 * 1024;
 static constexpr int kNHPlan = 6;
 static size_t ringfr_plan_smem(int ring, int sbuf, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 +
+    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 + 1024 * 12 +
            (size_t)nstage * ch * ((size_t)kp * 2 + 12);
 }
 
@@ -778,7 +813,7 @@ cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const in
 static constexpr int kNH = 6;   // RINGFR helper warps
 
 static size_t ringfr_smem_bytes(int ring, int sbuf, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 +
+    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 + 1024 * 12 +
            (size_t)nstage * ch * ((size_t)kp * 2 + 12);
 }
 
@@ -815,7 +850,7 @@ cudaError_t launch_moebius_ringfr(const DevPoset &P, const RingDFPlan &R, const 
     if (e != cudaSuccess) return e;
     void *args[] = {&a};
     launches_add(1);
-    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNH + 2)), args, smem, s);
+    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNH + 3)), args, smem, s);
 }
 
 cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
