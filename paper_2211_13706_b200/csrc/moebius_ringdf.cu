@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     if (tid == 0) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
         for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
-        for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 32);
+        for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 1);
         asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
                      : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -457,9 +457,13 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         }
         long long t_pre = 0;
         if (PROF) t_pre = clock64();
-        // publish: every lane releases its own ring stores
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
-                     : "memory");
+        // publish: __syncwarp orders the lanes' ring stores before lane 0's
+        // single release-arrive (one arrival per level: the sync unit
+        // processes arrivals one at a time)
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
+                         : "memory");
         if (lane == 0) {
             asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
             if (PROF && b == 0) {
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(32 * (kNH + 3)) k_moeb_ringfr(RDFArgs a) {
     if (tid == 0) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
         for (int s2 = 0; s2 < a.nstage; s2++) mbar_init(&bars[s2], 1);
-        for (int s2 = 0; s2 < 2 * kLB; s2++) mbar_init(&lvlbar[s2], 32);
+        for (int s2 = 0; s2 < 2 * kLB; s2++) mbar_init(&lvlbar[s2], 1);
         asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
                      : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -724,9 +728,11 @@ __global__ void __launch_bounds__(32 * (kNH + 3)) k_moeb_ringfr(RDFArgs a) {
             }
         }
         __syncwarp();
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
-                     : "memory");
-        if (lane == 0) df_rel(ctrl + 4, hi);   // ranks < hi final (producer, writer)
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
+                         : "memory");
+            df_rel(ctrl + 4, hi);   // ranks < hi final (producer, writer)
+        }
         R = Rn;
         // fbuf slots of the next level must have been drained
         if (nhi - FB > drained) {
