@@ -680,7 +680,7 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)
-        if (value < 0 || value > 2) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0..3");
         set_gather_variant((int)value);
         return POSET_OK;
     }

@@ -593,15 +593,20 @@ __device__ __forceinline__ void ld4_if_ne(u64 (&v)[4], const void *p, int32_t a,
                  : "r"(a), "r"(b), "l"(p));
 }
 
-template <typename T, int KCH>
-__global__ void __launch_bounds__(256, 2) k_gather_r4(const int32_t *__restrict__ M, int32_t n,
+template <typename T, int KCH, int KC = 4, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_gather_r4(const int32_t *__restrict__ M, int32_t n,
                                                       int32_t k, const T *__restrict__ F,
                                                       T *__restrict__ out,
                                                       const int32_t *__restrict__ rank_user,
                                                       int64_t row_lo, int64_t row_hi, int32_t B,
                                                       int G32, int mode) {
-    constexpr int TS = 4, KC = 4, TRW = 16;   // ranks per lane, chains per step, ranks per warp
-    __shared__ __align__(16) int32_t sid[8][TRW][KCH];
+    constexpr int TS = 4, TRW = 16;   // ranks per lane, ranks per warp; KC chains per step
+    // rank-major id tile, row stride KCH + 2 words: the staging writes (lanes
+    // over 16 ranks x 2 chains) and the 4 lane groups' 8-byte reads of rows
+    // 4q + ts both fall on distinct banks (ncu: the unpadded 64-word stride
+    // made shared-memory wavefronts the bulk of the L1 data-pipe load)
+    constexpr int SW = KCH + 2;
+    __shared__ __align__(16) int32_t sid[8][TRW][SW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane >> 3, cq = lane & 7;
     const int cg = (int)(blockIdx.x % G32);
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_r4(const int32_t *__restrict_
     const int col0 = cg * 32 + cq * 4;
     const char *Fb = reinterpret_cast<const char *>(F + col0);
     const unsigned rowbytes = (unsigned)B * sizeof(T);
-    int32_t (*S)[KCH] = sid[warp];
+    int32_t (*S)[SW] = sid[warp];
     T acc[TS][4];
 #pragma unroll
     for (int ts = 0; ts < TS; ts++)
@@ -639,17 +644,25 @@ __global__ void __launch_bounds__(256, 2) k_gather_r4(const int32_t *__restrict_
             for (int u = 0; u < KC; u++) prev[u] = -1;   // never an index: first rank loads
 #pragma unroll
             for (int ts = 0; ts < TS; ts++) {
-                const int4 id4 = *reinterpret_cast<const int4 *>(&S[q * TS + ts][jj]);
-                const int32_t id[KC] = {id4.x, id4.y, id4.z, id4.w};
+                int32_t id[KC];
+#pragma unroll
+                for (int u = 0; u < KC; u += 2) {
+                    const int2 id2 = *reinterpret_cast<const int2 *>(&S[q * TS + ts][jj + u]);
+                    id[u] = id2.x;
+                    id[u + 1] = id2.y;
+                }
 #pragma unroll
                 for (int u = 0; u < KC; u++) {
                     ld4_if_ne(v[u], Fb + (size_t)(unsigned)id[u] * rowbytes, id[u], prev[u]);
                     prev[u] = id[u];
                 }
 #pragma unroll
-                for (int c = 0; c < 4; c++)
-                    acc[ts][c] += (from_bits<T>(v[0][c]) + from_bits<T>(v[1][c])) +
-                                  (from_bits<T>(v[2][c]) + from_bits<T>(v[3][c]));
+                for (int c = 0; c < 4; c++) {
+                    T t = from_bits<T>(v[0][c]);
+#pragma unroll
+                    for (int u = 1; u < KC; u++) t += from_bits<T>(v[u][c]);
+                    acc[ts][c] += t;
+                }
             }
         }
     }
@@ -748,11 +761,15 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
                             int64_t B, int mode, void *partial, int num_sms, cudaStream_t s) {
     int S = gather_slices(P, hi - lo, B, num_sms);
     if (S > 1 && !partial) S = 1;
-    if (B % 32 == 0 && S == 1 && gather_variant() == 0) {
+    if (B % 32 == 0 && S == 1 && (gather_variant() == 0 || gather_variant() == 3)) {
         const int G32 = (int)(B / 32);
         const int64_t tiles = (hi - lo + 8 * 16 - 1) / (8 * 16);
-        k_gather_r4<T, 64><<<(unsigned)(tiles * G32), 256, 0, s>>>(
-            P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+        if (gather_variant() == 0)   // 2 chains per step: fewer registers, 3 CTAs per SM (measured best)
+            k_gather_r4<T, 64, 2, 3><<<(unsigned)(tiles * G32), 256, 0, s>>>(
+                P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+        else
+            k_gather_r4<T, 64><<<(unsigned)(tiles * G32), 256, 0, s>>>(
+                P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         COUNT_LAUNCH(1);
         return cudaGetLastError();
     }
