@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--moebius-kernel", default="auto", choices=MOEB_NAMES)
     ap.add_argument("--gather-variant", type=int, default=0, help="dense gather kernel for B%%32==0 (tuning)")
+    ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -222,6 +223,8 @@ def main():
     kern = MOEB_NAMES.index(args.moebius_kernel)
     P.set_option("moebius_kernel", kern)
     P.set_option("gather_variant", args.gather_variant)
+    if args.ring_debug:
+        P.set_option("ring_debug", args.ring_debug)
     f_host = wl.values(seed=1 + rank)
     x = torch.from_numpy(f_host).cuda()
     g = torch.empty_like(x)
