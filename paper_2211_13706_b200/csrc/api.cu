@@ -151,17 +151,17 @@ static poset_status finish_setup(poset_s *h) {
         int32_t *d_slot_rank = nullptr, *d_level = nullptr;
         CK(upload(&d_slot_rank, H.slot_rank));
         CK(upload(&d_level, H.level));
-        unsigned reach = 0, near3[3] = {0, 0, 0}, counts2[2] = {0, 0};
+        unsigned reach = 0, near3[3] = {0, 0, 0}, counts3[3] = {0, 0, 0};
         cudaError_t e = launch_reach_max(P, d_slot_rank, (unsigned *)h->d_count, 0);
         if (e == cudaSuccess) e = cudaMemcpy(&reach, h->d_count, sizeof reach, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess) e = launch_near_max(P, d_level, d_slot_rank, (unsigned *)h->d_count, 0);
         if (e == cudaSuccess) e = cudaMemcpy(near3, h->d_count, sizeof near3, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess) e = launch_df_counts(P, d_level, d_slot_rank, (unsigned *)h->d_count, 0);
-        if (e == cudaSuccess) e = cudaMemcpy(counts2, h->d_count, sizeof counts2, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(counts3, h->d_count, sizeof counts3, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) { cudaFree(d_slot_rank); cudaFree(d_level); CK(e); }
         ring_plan(H.n, H.k, H.ell, H.max_level_width, reach, h->ring);
         ringws_plan(H.n, H.k, H.max_level_width, reach, near3, h->rws);
-        ringdf_plan(H.n, H.k, H.max_level_width, reach, counts2, h->rdf);
+        ringdf_plan(H.n, H.k, H.max_level_width, reach, counts3, h->rdf);
         const int64_t npad = ((int64_t)H.n + 255) / 256 * 256;   // common to all plans
         h->ring.npad = npad;
         h->rws.npad = npad;
@@ -232,7 +232,7 @@ static poset_status finish_setup(poset_s *h) {
                    (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0) +
                    (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
-    I.ringdf = h->rdf.ok ? (h->rdf.fr_ok ? 3 : 1) : 0;   // bit 1: RINGFR available
+    I.ringdf = h->rdf.ok ? 1 : 0;   // bit 1 (RINGFR, removed) stays clear
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
@@ -414,19 +414,8 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
-    if (which == MOEB_RINGFR) {
-        if (!h->rdf.ok || !h->rdf.fr_ok)
-            return fail(POSET_EINVAL, "poset_moebius: the RINGFR schedule does not fit this poset; use AUTO");
-        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
-        if (st) return st;
-        {
-            PhaseTimer t(h, POSET_PH_PERM, s);
-            CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
-        }
-        PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        CK(launch_moebius_ringfr(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
-        return POSET_OK;
-    }
+    if (which == MOEB_RINGFR)
+        return fail(POSET_EINVAL, "poset_moebius: the RINGFR schedule was removed (slower than RINGDF); use AUTO");
     if (which == MOEB_RINGDF) {
         if (!h->rdf.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
@@ -662,11 +651,6 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
                 return fail(POSET_EINVAL, "ringws_lpeo must leave 8 or 16 far entries per lane");
             h->rws.lpeo = (int32_t)value;
         }
-        return POSET_OK;
-    }
-    if (!strcmp(key, "ringdf_nwc")) {   // RINGDF consumer warps (tuning)
-        if (!h->rdf.ok || (value != 4 && value != 8)) return fail(POSET_EINVAL, "ringdf_nwc is 4 or 8");
-        h->rdf.nwc = (int32_t)value;
         return POSET_OK;
     }
     if (!strcmp(key, "ring_debug")) {   // timing experiments only (bit 0: results NOT valid,

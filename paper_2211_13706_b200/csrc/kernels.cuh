@@ -129,11 +129,9 @@ cudaError_t launch_moebius_ringws(const DevPoset &P, const RingWSPlan &R, const 
 // pipeline, near / mid / far dependencies ----
 struct RingDFPlan {
     bool ok = false;
-    int32_t nn = 0, nm = 0, fe = 0;   // near / mid / far row entries
+    int32_t nn = 0, nm = 0, fe = 0;   // near / mid / far row entries (far: bank-coloured, /16)
     int32_t kp = 0, ring = 0, ch = 0, nstage = 0;
-    int32_t nwc = 8;                  // consumer warps (4 or 8)
-    int32_t sbuf = 0;                 // RINGFR S_old buffer entries
-    bool fr_ok = false;               // RINGFR fits shared memory
+    int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only
     unsigned long long *dbg = nullptr;
@@ -141,15 +139,12 @@ struct RingDFPlan {
     uint16_t *D = nullptr;
 };
 void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
-                 const unsigned counts2[2], RingDFPlan &R);
+                 const unsigned counts3[3], RingDFPlan &R);
 cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int32_t *slot_rank,
-                             unsigned *out2, cudaStream_t s);
+                             unsigned *out3, cudaStream_t s);   // near max, mid max, far colours
 cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *level,
                                 const int32_t *slot_rank, cudaStream_t s);
 cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
-// RINGFR: the same tables, critical path in one "fresh" warp, far/mid sums by helpers
-cudaError_t launch_moebius_ringfr(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
                                   int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
 
 // ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----

@@ -22,13 +22,14 @@
 // RING >= reach + 12 * max level width so no slot is overwritten while any
 // warp may still read it.
 //
-//   rows [npad][kp] uint16 ring slots (RING = the zero entry):
-//     [0, NN) near | [NN, NN+NM) mid | [NN+NM, NN+NM+FE) far (bank-sorted) | pn
+//   rows [npad][kp] uint16: see k_build_ringdf (mid | near | pn | counts |
+//   far, the far entries bank-coloured per half-warp)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -41,6 +42,7 @@ static constexpr int kNear = 2;    // level distance <= kNear: near
 static constexpr int kMid = 6;     // kNear < distance <= kMid: mid; beyond: far
 static constexpr int kLB = 16;     // level-completion mbarriers (ring), > kMid + 1
 static constexpr int kNP = 3;      // passes of 32 elements kept in registers per level
+static constexpr int kNWC = 8;     // consumer warps (levels round-robin)
 
 // ------------------------------------------------------------ setup -------
 // max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
@@ -70,77 +72,156 @@ __global__ void k_df_counts(const int32_t *__restrict__ M, int32_t n, int32_t k,
     }
 }
 
+// Row layout (uint16 entries; all but the counts word are byte offsets into
+// the ring, the zero entries RING .. RING+15 padding every segment):
+//   [0, NM) mid | [NM, NM+NN) near | pn | counts | pad to 16 B | far (fe)
+// counts = nnear | nmid << 5 | nf16 << 11, nf16 = far entries / 16 of the row's
+// half-warp group (the kernel loops to the warp maximum).
+__host__ __device__ constexpr int df_off_far(int nm, int nn) { return (2 * (nm + nn + 2) + 15) / 16 * 16; }
+
+// Far entries are ORDERED so that a warp's shared-memory loads hit distinct
+// banks: within each half-warp group (16 consecutive ranks of a level pass,
+// the lanes of one wavefront of 8-byte loads) every position j holds 16
+// distinct bank pairs (slot & 15).  This is an edge colouring of the
+// lanes x banks bipartite multigraph, done first-fit with 64-bit position
+// masks per bank -- except that lanes needing the same slot share a position
+// when they can (one address = a broadcast, no conflict; far dependencies of
+// one level's elements overlap heavily).  Free (lane, position) cells take
+// the zero entry of a bank nobody uses there.  WRITE = false only measures
+// the longest group (-> fe).
+template <bool WRITE>
 __global__ void __launch_bounds__(256) k_build_ringdf(
-    const int32_t *__restrict__ M, int32_t n, int32_t k, int32_t kp, int32_t nn, int32_t nm,
-    int32_t fe, int32_t ring, const int32_t *__restrict__ chain, const int32_t *__restrict__ slot,
+    const int32_t *__restrict__ M, int32_t n, int32_t k, const int32_t *__restrict__ lvl_ptr,
+    int32_t kp, int32_t nn, int32_t nm, int32_t fe, int32_t ring,
+    const int32_t *__restrict__ chain, const int32_t *__restrict__ slot,
     const int32_t *__restrict__ slot_rank, const int32_t *__restrict__ level,
-    uint16_t *__restrict__ D) {
-    extern __shared__ uint16_t tile[];   // raw [32][k+1] slots, class [32][k+1], out [32][kp]
+    uint16_t *__restrict__ D, unsigned *__restrict__ jmax) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     const int ks = k + 1;
-    uint16_t *raw = tile, *cls = tile + 32 * ks, *outr = tile + 64 * ks;
-    const int r0 = blockIdx.x * 32;
+    unsigned long long *posmask = reinterpret_cast<unsigned long long *>(dsm);   // [2][16][4]
+    unsigned long long *taken = posmask + 2 * 16 * 4;                              // [32][4]
+    uint16_t *raw = reinterpret_cast<uint16_t *>(taken + 32 * 4);                  // [32][ks] slots
+    uint16_t *cls = raw + 32 * ks;                                                 // [32][ks] classes
+    uint16_t *outr = cls + 32 * ks;                                                // [32][kp]
+    uint16_t *slotpos = outr + 32 * kp;   // [2][4096]: position + 1 of a slot already placed
+    for (int t = threadIdx.x; t < 2 * 4096; t += blockDim.x) slotpos[t] = 0;
+    __shared__ int jh[2];
+    const int L = blockIdx.x;
+    const int lo = lvl_ptr[L], hi = lvl_ptr[L + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int r = r0 + lane;
     const int mask = ring - 1;
-    for (int j = w; j < k; j += nw) {
-        int dep = -1;
-        if (r < n) {
-            const int32_t s = M[(size_t)j * n + r];
-            if (s != n && chain[r] != j) dep = slot_rank[s];
+    const int ofar = df_off_far(nm, nn) / 2;
+    for (int r0 = lo; r0 < hi; r0 += 32) {
+        const int nr = min(32, hi - r0);
+        const int r = r0 + lane;
+        for (int j = w; j < k; j += nw) {
+            int dep = -1;
+            if (lane < nr) {
+                const int32_t s = M[(size_t)j * n + r];
+                if (s != n && chain[r] != j) dep = slot_rank[s];
+            }
+            raw[lane * ks + j] = (uint16_t)(dep >= 0 ? (dep & mask) : 0);
+            int c = 3;   // 0 near, 1 mid, 2 far, 3 none
+            if (dep >= 0) {
+                const int32_t ld = level[r] - level[dep];
+                c = ld <= kNear ? 0 : ld <= kMid ? 1 : 2;
+            }
+            cls[lane * ks + j] = (uint16_t)c;
         }
-        raw[lane * ks + j] = (uint16_t)(dep >= 0 ? (dep & mask) : ring);   // slot; bytes on output
-        int c = 3;   // 0 near, 1 mid, 2 far, 3 none
-        if (dep >= 0) {
-            const int32_t ld = level[r] - level[dep];
-            c = ld <= kNear ? 0 : ld <= kMid ? 1 : 2;
-        }
-        cls[lane * ks + j] = (uint16_t)c;
-    }
-    __syncthreads();
-    if (w == 0) {
-        const uint16_t *in = raw + lane * ks, *cl = cls + lane * ks;
-        uint16_t *out = outr + lane * kp;
-        int nnear = 0, nmid = 0, cnt[16], pos[16], acc = 0;
+        __syncthreads();
+        if (w == 1 && (lane & 15) == 0) {
+            // first-fit colouring of half-warp group h (ranks r0+16h ..)
+            const int h = lane >> 4, nh = min(16, nr - 16 * h);
+            unsigned long long *pm = posmask + h * 64;
+            uint16_t *sp = slotpos + h * 4096;
+            for (int t = 0; t < 64; t++) pm[t] = 0ull;
+            int J = 0;
+            for (int i = 0; i < nh; i++) {
+                const int ln = 16 * h + i;
+                unsigned long long tk[4] = {0ull, 0ull, 0ull, 0ull};
+                for (int j = 0; j < k; j++) {
+                    if (cls[ln * ks + j] != 2) continue;
+                    const int s = raw[ln * ks + j], b = s & 15;
+                    int pos = (int)sp[s] - 1;
+                    if (pos < 0 || ((tk[pos >> 6] >> (pos & 63)) & 1ull)) {
+                        pos = 256;
 #pragma unroll
-        for (int c = 0; c < 16; c++) cnt[c] = 0;
-        for (int j = 0; j < k; j++) {
-            const int s = in[j];
-            if (cl[j] == 0) { if (nnear < nn) out[nnear] = (uint16_t)s; nnear++; }
-            else if (cl[j] == 1) { if (nmid < nm) out[nn + nmid] = (uint16_t)s; nmid++; }
-            else if (cl[j] == 2) cnt[(s - r) & 15]++;
-        }
-        for (int j = nnear; j < nn; j++) out[j] = (uint16_t)ring;
-        for (int j = nmid; j < nm; j++) out[nn + j] = (uint16_t)ring;
+                        for (int q = 0; q < 4; q++) {
+                            const unsigned long long fr = ~(pm[b * 4 + q] | tk[q]);
+                            if (pos == 256 && fr) pos = 64 * q + __ffsll((long long)fr) - 1;
+                        }
+                        if (pos >= 256) { J = 1 << 20; continue; }   // cannot happen for k <= 256
+                        pm[b * 4 + (pos >> 6)] |= 1ull << (pos & 63);
+                        if (!sp[s]) sp[s] = (uint16_t)(pos + 1);
+                    }
+                    tk[pos >> 6] |= 1ull << (pos & 63);
+                    if (WRITE && pos < fe) outr[ln * kp + ofar + pos] = (uint16_t)s;
+                    J = max(J, pos + 1);
+                }
 #pragma unroll
-        for (int c = 0; c < 16; c++) { pos[c] = acc; acc += cnt[c]; }
-        for (int j = 0; j < k; j++) {
-            if (cl[j] != 2) continue;
-            const int s = in[j];
-            const int c = (s - r) & 15;
-#pragma unroll
-            for (int cc = 0; cc < 16; cc++)
-                if (cc == c) out[nn + nm + pos[cc]++] = (uint16_t)s;
+                for (int q = 0; q < 4; q++) taken[ln * 4 + q] = tk[q];
+            }
+            if (!WRITE) {
+                atomicMax(jmax, (unsigned)J);
+            } else {
+                // free cells: the zero entry of a bank not used at that
+                // position (one address for all of them: a broadcast)
+                for (int pos = 0; pos < fe; pos++) {
+                    unsigned used = 0;
+                    for (int b = 0; b < 16; b++) used |= (unsigned)((pm[b * 4 + (pos >> 6)] >> (pos & 63)) & 1ull) << b;
+                    const int t = used == 0xffffu ? 0 : __ffs(~used & 0xffffu) - 1;
+                    for (int i = 0; i < nh; i++) {
+                        const int ln = 16 * h + i;
+                        if ((taken[ln * 4 + (pos >> 6)] >> (pos & 63)) & 1ull) continue;
+                        outr[ln * kp + ofar + pos] = (uint16_t)(ring + t);
+                    }
+                }
+                jh[h] = (J + 15) / 16;
+            }
+            for (int i = 0; i < nh; i++)   // clear the slot map for the next pass
+                for (int j = 0; j < k; j++)
+                    if (cls[(16 * h + i) * ks + j] == 2) sp[raw[(16 * h + i) * ks + j]] = 0;
         }
-        for (int j = nn + nm + acc; j < kp; j++) out[j] = (uint16_t)ring;
-        int pn = -1;
-        if (r < n) {
+        if (WRITE && w == 0 && lane < nr) {
+            const uint16_t *in = raw + lane * ks, *cl = cls + lane * ks;
+            uint16_t *out = outr + lane * kp;
+            int nnear = 0, nmid = 0;
+            for (int j = 0; j < k; j++) {
+                const int s = in[j];
+                if (cl[j] == 0) { if (nnear < nn) out[nm + nnear] = (uint16_t)s; nnear++; }
+                else if (cl[j] == 1) { if (nmid < nm) out[nmid] = (uint16_t)s; nmid++; }
+            }
+            for (int j = nnear; j < nn; j++) out[nm + j] = (uint16_t)ring;
+            for (int j = nmid; j < nm; j++) out[j] = (uint16_t)ring;
+            for (int j = nm + nn + 2; j < ofar; j++) out[j] = (uint16_t)ring;
+            for (int j = ofar + fe; j < kp; j++) out[j] = (uint16_t)ring;
+            int pn = -1;
             const int32_t s = slot[r];
             if (s > 0) {
                 const int32_t p = slot_rank[s - 1];
                 if (chain[p] == chain[r]) pn = p;
             }
+            out[nm + nn] = (uint16_t)(pn >= 0 ? (pn & mask) : ring);
         }
-        out[nn + nm + fe] = (uint16_t)(pn >= 0 ? (pn & mask) : ring);
-        out[nn + nm + fe + 1] = (uint16_t)(min(nnear, nn) | (min(nmid, nm) << 8));
-    }
-    __syncthreads();
-    // ring slots -> byte offsets into the ring (slot * 8; RING * 8 < 65536 by
-    // the plan), except the counts word
-    const int64_t base = (int64_t)r0 * kp;
-    for (int t = threadIdx.x; t < 32 * kp; t += blockDim.x) {
-        const int j = t % kp;
-        const uint16_t v = outr[t];
-        D[base + t] = j == nn + nm + fe + 1 ? v : (uint16_t)(v * 8);
+        __syncthreads();
+        if (WRITE) {
+            if (w == 0 && lane < nr) {
+                int nnear = 0, nmid = 0;
+                for (int j = 0; j < k; j++) { nnear += cls[lane * ks + j] == 0; nmid += cls[lane * ks + j] == 1; }
+                outr[lane * kp + nm + nn + 1] =
+                    (uint16_t)(min(nnear, nn) | (min(nmid, nm) << 5) | (jh[lane >> 4] << 11));
+            }
+            __syncthreads();
+            // ring slots -> byte offsets (slot * 8; (RING + 16) * 8 <= 65536 by
+            // the plan), except the counts word
+            const int64_t base = (int64_t)r0 * kp;
+            for (int t = threadIdx.x; t < nr * kp; t += blockDim.x) {
+                const int j = t % kp;
+                const uint16_t v = outr[t];
+                D[base + t] = j == nm + nn + 1 ? v : (uint16_t)(v * 8);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -155,7 +236,6 @@ struct RDFArgs {
     int32_t n, kp, ell, B;
     int32_t ring_mask;
     int32_t lg_ch, nstage;
-    int32_t sbuf;               // RINGFR: S_old buffer entries (power of two)
     int32_t skip_far;           // timing experiment only (results invalid): bit 0 far, bit 1 mid,
                                 // bit 2 near sums skipped
     unsigned long long *dbg;    // PROF instantiation only: [0] Σ ready->publish, [1] Σ publish->ready
@@ -171,6 +251,19 @@ __device__ __forceinline__ u64 df_lds64(unsigned addr) {
     u64 v;
     asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
     return v;
+}
+// predicated 8-byte shared load (0 when p == 0) / store: no branch
+__device__ __forceinline__ u64 df_ldp64(unsigned addr, unsigned p) {
+    u64 v;
+    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.shared.b64 %0, [%1];\n}"
+                 : "=l"(v)
+                 : "r"(addr), "r"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void df_stp64(unsigned addr, u64 v, unsigned p) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.shared.b64 [%0], %1;\n}" ::"r"(addr), "l"(v), "r"(p)
+                 : "memory");
 }
 __device__ __forceinline__ unsigned lds32u(unsigned addr) {
     unsigned v;
@@ -267,15 +360,50 @@ __device__ __forceinline__ u64 df_bits<u64>(u64 x) { return x; }
 template <>
 __device__ __forceinline__ u64 df_bits<double>(double x) { return (u64)__double_as_longlong(x); }
 
-template <typename T, int NN, int NM, int FE, int kNWC, bool PROF = false>
+// value pinned in a register at this point of the program: the compiler may
+// not recompute it later (used to keep address / partial-sum arithmetic off
+// the post-wait critical path)
+__device__ __forceinline__ void df_pin(unsigned &x) { asm volatile("" : "+r"(x)); }
+__device__ __forceinline__ void df_pin(u64 &x) { asm volatile("" : "+l"(x)); }
+__device__ __forceinline__ void df_pin(double &x) { asm volatile("" : "+d"(x)); }
+
+// NN/2 words of near slots (two 16-bit byte offsets per word)
+template <int NN>
+__device__ __forceinline__ void df_near_words(unsigned addr, unsigned (&w)[NN / 2]) {
+    if constexpr (NN == 4) {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+    } else {
+#pragma unroll
+        for (int q = 0; q < NN / 8; q++) {
+            const uint4 v = df_lds128(addr + 16 * q);
+            w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+        }
+    }
+}
+// Σ ring[slot] over E row entries, read one by one (the rare serial passes)
+template <typename T, int E>
+__device__ __forceinline__ T df_sum_u16(unsigned ring_base, unsigned row) {
+    T acc = T(0);
+#pragma unroll 4
+    for (int j = 0; j < E; j++) {
+        unsigned short o;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(o) : "r"(row + 2 * j));
+        acc += bits_to<T>(df_lds64(ring_base + (unsigned)o));
+    }
+    return acc;
+}
+
+template <typename T, int NN, int NM, bool PROF = false>
 __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
+    // row layout, byte offsets (rows are [kp] uint16): mid | near | pn, counts | far
+    constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN), OFF_FAR = df_off_far(NM, NN);
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
     const int ch = 1 << a.lg_ch;
-    const unsigned ring_base = smem_u32(smem);                            // RING + 2 entries
-    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);
+    const unsigned ring_base = smem_u32(smem);                            // RING + 16 entries
+    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 16) * 8);
     const unsigned ctrl = smem_u32(bars + ((a.nstage + kLB + 1) & ~1));   // ready, done_rank
-    unsigned char *stage0 = smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + kLB + 1) & ~1) + 16;
+    unsigned char *stage0 = smem + (size_t)(RING + 16) * 8 + 8 * ((a.nstage + kLB + 1) & ~1) + 16;
     const unsigned stage_base = smem_u32(stage0);
     const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
     const unsigned sbytes = dbytes + gbytes + ubytes;
@@ -284,8 +412,9 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
     const int32_t nchunks = (int32_t)(a.npad >> a.lg_ch);
 
+    if (tid < 16)   // the zero entries, one per bank pair
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(RING + tid) * 8), "l"(0ull) : "memory");
     if (tid == 0) {
-        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
         for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
         for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 1);
         asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
@@ -329,14 +458,16 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     }
 
     // ------------------------------------------------------- consumers ----
-    // Level completion is published on a ring of kLB mbarriers: the 32 lanes
-    // of the warp that owns level L arrive (release) on lvlbar[L % kLB] once
-    // their ring stores are issued; a waiter for "level L done" try_waits
-    // (acquire) on the phase (L / kLB) & 1.  Levels finish in order, so "L
-    // done" means every level <= L is done, and no waiter ever looks more
-    // than kMid + 1 < kLB levels back, so parities cannot alias.
+    // Level completion is published on a ring of kLB mbarriers: lane 0 of the
+    // warp that owns level L arrives (release, after a __syncwarp that orders
+    // the lanes' ring stores) on lvlbar[L % kLB]; a waiter for "level L done"
+    // try_waits (acquire) on the phase (L / kLB) & 1.  Levels finish in
+    // order, so "L done" means every level <= L is done, and no waiter ever
+    // looks more than kMid + 1 < kLB levels back, so parities cannot alias.
     T *f = reinterpret_cast<T *>(a.f);
     u64 *lvlbar = bars + a.nstage;   // kLB barriers after the stage barriers
+    const unsigned lvl_u32 = smem_u32(lvlbar);
+    const unsigned zero_off = (unsigned)RING * 8u;   // byte offset of the zero entry
     __shared__ unsigned long long prof[8];
     __shared__ volatile unsigned long long prof_last;
     long long t_ready = 0;
@@ -371,7 +502,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         T gx[kNP], sp[kNP];
         int32_t u[kNP];
         unsigned rowa[kNP], pn[kNP], cnt[kNP];
-        uint4 nw[kNP][NN / 8];
+        unsigned nw[kNP][NN / 2];
 #pragma unroll
         for (int p = 0; p < kNP; p++) {
             if (p < np) {
@@ -382,91 +513,137 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 rowa[p] = st + off * (unsigned)a.kp * 2;
                 gx[p] = bits_to<T>(df_lds64(st + dbytes + off * 8));
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + dbytes + gbytes + off * 4));
-                unsigned pc;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pc) : "r"(rowa[p] + 2 * (NN + NM + FE)));
+                const unsigned pc = lds32u(rowa[p] + OFF_PN);
                 pn[p] = pc & 0xffffu;
-                cnt[p] = pc >> 16;   // near count | mid count << 8
-#pragma unroll
-                for (int q = 0; q < NN / 8; q++) nw[p][q] = df_lds128(rowa[p] + 16 * q);
+                cnt[p] = pc >> 16;   // near count | mid count << 5 | far chunks << 11
+                df_near_words<NN>(rowa[p] + OFF_NEAR, nw[p]);
                 u[p] = e < hi ? u[p] : -1;
+            } else {
+                gx[p] = T(0);
+                u[p] = -1;
+                rowa[p] = pn[p] = cnt[p] = 0;
+#pragma unroll
+                for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
             }
         }
         wait_level(L - kMid - 1);   // far: levels <= L-7
 #pragma unroll
-        for (int p = 0; p < kNP; p++)
-            if (p < np) sp[p] = (a.skip_far & 1) ? T(0) : df_sum<T, FE>(ring_base, rowa[p] + 2 * (NN + NM));
+        for (int p = 0; p < kNP; p++) {
+            if (p < np) {
+                // far entries in chunks of 16, to the longest row of the warp
+                const unsigned nf = (a.skip_far & 1) ? 0u : __reduce_max_sync(0xffffffffu, cnt[p] >> 11);
+                T acc = T(0);
+                for (unsigned c = 0; c < nf; c++) acc += df_sum<T, 16>(ring_base, rowa[p] + OFF_FAR + 32 * c);
+                sp[p] = acc;
+            }
+        }
         wait_level(L - kNear - 1);  // mid: levels <= L-3
 #pragma unroll
         for (int p = 0; p < kNP; p++) {
             if (p < np) {
                 uint4 mw[NM / 8];
 #pragma unroll
-                for (int q = 0; q < NM / 8; q++) mw[q] = df_lds128(rowa[p] + 2 * NN + 16 * q);
-                if (!(a.skip_far & 2)) sp[p] += df_sum_wc<T, NM>(ring_base, mw, (int)(cnt[p] >> 8));
+                for (int q = 0; q < NM / 8; q++) mw[q] = df_lds128(rowa[p] + 16 * q);
+                if (!(a.skip_far & 2)) sp[p] += df_sum_wc<T, NM>(ring_base, mw, (int)((cnt[p] >> 5) & 63u));
             }
         }
-        long long t_wait = 0;
-        if (PROF) t_wait = clock64();
-        wait_level(L - 1);          // near: the critical path
-        if (PROF) {
-            t_ready = clock64();
-            if (lane == 0 && b == 0 && L > 0) {
-                const long long tp = (long long)prof_last;
-                if (t_wait > tp) { prof[2] += t_wait - tp; prof[3] += 1; }
-                else prof[1] += t_ready - tp;
-            }
-        }
-        T fo[kNP];
+        // Everything the critical path needs is formed (and pinned in
+        // registers) before the near wait: gx - (far + mid), the absolute ring
+        // addresses of the near slots (padding = the zero entry, so the loads
+        // need no predicates), the ring store address and predicate and the
+        // barrier address.  After the wait: NN loads per pass, the add tree,
+        // one subtract, a predicated store, __syncwarp and the arrive.
+        unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
+        df_pin(lvl_addr);
+        T gs[kNP], Fx[kNP];
+        unsigned na[kNP][NN], sa[kNP], stp[kNP];
 #pragma unroll
         for (int p = 0; p < kNP; p++) {
-            if (p < np) {
-                const T sn = (a.skip_far & 4) ? T(0) : df_sum_wc<T, NN>(ring_base, nw[p], (int)(cnt[p] & 0xffu));
+            gs[p] = p < np ? gx[p] - sp[p] : T(0);
+            df_pin(gs[p]);
+            sa[p] = ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u;
+            stp[p] = (p < np && u[p] >= 0) ? 1u : 0u;
+            df_pin(sa[p]);
+            df_pin(stp[p]);
+#pragma unroll
+            for (int q = 0; q < NN / 2; q++) {
+                const unsigned w = (a.skip_far & 4) ? (zero_off | (zero_off << 16)) : nw[p][q];
+                na[p][2 * q] = ring_base + (w & 0xffffu);
+                na[p][2 * q + 1] = ring_base + (w >> 16);
+                df_pin(na[p][2 * q]);
+                df_pin(na[p][2 * q + 1]);
+            }
+        }
+        // the level tail for NPX passes (NPX = 1: the common single-pass
+        // level, no code for the other passes in the critical path)
+        auto tail = [&](auto npx) {
+            constexpr int NPX = decltype(npx)::value;
+            long long t_wait = 0;
+            if (PROF) t_wait = clock64();
+            wait_level(L - 1);          // near: the critical path
+            if (PROF) {
+                t_ready = clock64();
+                if (lane == 0 && b == 0 && L > 0) {
+                    const long long tp = (long long)prof_last;
+                    if (t_wait > tp) { prof[2] += t_wait - tp; prof[3] += 1; }
+                    else prof[1] += t_ready - tp;
+                }
+            }
+            T v[NPX][NN];
+#pragma unroll
+            for (int p = 0; p < NPX; p++)
+#pragma unroll
+                for (int j = 0; j < NN; j++) v[p][j] = bits_to<T>(df_lds64(na[p][j]));
+#pragma unroll
+            for (int p = 0; p < NPX; p++) {
+#pragma unroll
+                for (int st = 1; st < NN; st <<= 1)
+#pragma unroll
+                    for (int j = 0; j < NN; j += 2 * st) v[p][j] += v[p][j + st];
+                Fx[p] = gs[p] - v[p][0];
                 if (PROF && p == 0 && lane == 0 && b == 0) {
-                    // force the near sum to complete before the stamp
-                    asm volatile("" ::"l"(df_bits<T>(sn)));
+                    asm volatile("" ::"l"(df_bits<T>(Fx[0])));   // the near sum completes before the stamp
                     prof[7] += clock64() - t_ready;
                 }
-                const T Fx = gx[p] - (sp[p] + sn);
-                fo[p] = Fx - bits_to<T>(df_lds64(ring_base + pn[p]));
-                if (u[p] >= 0)
-                    asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8),
-                                 "l"(df_bits<T>(Fx))
-                                 : "memory");
             }
-        }
-        // passes beyond kNP (levels wider than 32 * kNP): serially, all deps done
-        for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
-            const int32_t e = base + lane;
-            const int32_t ee = e < hi ? e : base;
-            const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
-            const unsigned off = (unsigned)(ee & (ch - 1));
-            const unsigned row = st + off * (unsigned)a.kp * 2;
-            const T g1 = bits_to<T>(df_lds64(st + dbytes + off * 8));
-            int32_t u1;
-            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + dbytes + gbytes + off * 4));
-            unsigned short p16;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(p16) : "r"(row + 2 * (NN + NM + FE)));   // pads load zero
-            const T Fx = g1 - (df_sum<T, FE>(ring_base, row + 2 * (NN + NM)) + df_sum<T, NM>(ring_base, row + 2 * NN) +
-                               df_sum<T, NN>(ring_base, row));
-            if (e < hi) {
-                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
-                             "l"(df_bits<T>(Fx))
-                             : "memory");
-                f[(size_t)u1 * a.B + b] = Fx - bits_to<T>(df_lds64(ring_base + (unsigned)p16));
+#pragma unroll
+            for (int p = 0; p < NPX; p++) df_stp64(sa[p], df_bits<T>(Fx[p]), stp[p]);
+            if (NPX == kNP) {
+                // passes beyond kNP (levels wider than 32 * kNP): serially, all deps done
+                for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
+                    const int32_t e = base + lane;
+                    const int32_t ee = e < hi ? e : base;
+                    const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
+                    const unsigned off = (unsigned)(ee & (ch - 1));
+                    const unsigned row = st + off * (unsigned)a.kp * 2;
+                    const T g1 = bits_to<T>(df_lds64(st + dbytes + off * 8));
+                    int32_t u1;
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + dbytes + gbytes + off * 4));
+                    const unsigned pc1 = lds32u(row + OFF_PN);
+                    const unsigned p16 = pc1 & 0xffffu;
+                    T s1 = df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
+                    for (unsigned c = 0; c < (pc1 >> 27); c++) s1 += df_sum<T, 16>(ring_base, row + OFF_FAR + 32 * c);
+                    const T F1 = g1 - s1;
+                    if (e < hi) {
+                        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
+                                     "l"(df_bits<T>(F1))
+                                     : "memory");
+                        f[(size_t)u1 * a.B + b] = F1 - bits_to<T>(df_lds64(ring_base + p16));
+                    }
+                }
             }
-        }
-        long long t_pre = 0;
-        if (PROF) t_pre = clock64();
-        // publish: __syncwarp orders the lanes' ring stores before lane 0's
-        // single release-arrive (one arrival per level: the sync unit
-        // processes arrivals one at a time)
-        __syncwarp();
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
-                         : "memory");
-        if (lane == 0) {
-            asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"(ctrl + 4), "r"(hi) : "memory");
-            if (PROF && b == 0) {
+            long long t_pre = 0;
+            if (PROF) t_pre = clock64();
+            // publish: __syncwarp orders the lanes' ring stores before lane 0's
+            // single release-arrive; lane 0 also advances done_rank (producer)
+            __syncwarp();
+            asm volatile(
+                "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
+                "@q mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
+                "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
+                "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
+                : "memory");
+            if (PROF && lane == 0 && b == 0) {
                 const long long t = clock64();
                 prof[0] += t - t_ready;
                 prof[4] += 1;
@@ -474,10 +651,16 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 prof[6] += np;
                 prof_last = (unsigned long long)t;
             }
-        }
+        };
+        if (np <= 1)
+            tail(std::integral_constant<int, 1>{});
+        else
+            tail(std::integral_constant<int, kNP>{});
+        // f(x) = F(x) - F(next below on the chain), after the publish, off the
+        // critical path (the pn slot stays live: RING >= reach + 18 wmax)
 #pragma unroll
         for (int p = 0; p < kNP; p++)
-            if (p < np && u[p] >= 0) f[(size_t)u[p] * a.B + b] = fo[p];
+            if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
     }
     if (PROF) {
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
@@ -486,318 +669,58 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Schedule RINGFR ("fresh warp"): the same tables, but the level-by-level
-// critical path stays inside ONE warp (hand-off between levels = __syncwarp;
-// the near dependencies, levels L-1 and L-2, were written by this warp
-// itself), and kNH helper warps compute each element's far + mid sum
-// S_old(x) ahead of time: helper h owns levels L ≡ h (mod kNH), sums the far
-// part once level L-7 is done and the mid part once level L-3 is done, writes
-// S_old into a shared buffer and arrives on sold_bar[L % kLB].  The fresh warp
-// publishes level completion on lvl_bar[L % kLB] (arrive.release by its 32
-// lanes) for the helpers; it normally finds sold_bar[L] already complete.
-template <typename T, int NN, int NM, int FE, int kNH>
-__global__ void __launch_bounds__(32 * (kNH + 3)) k_moeb_ringfr(RDFArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int RING = a.ring_mask + 1;
-    const int ch = 1 << a.lg_ch;
-    const unsigned ring_base = smem_u32(smem);
-    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(RING + 2) * 8);   // nstage + 2 * kLB
-    u64 *lvlbar = bars + a.nstage, *soldbar = lvlbar + kLB;
-    const unsigned ctrl = smem_u32(bars + ((a.nstage + 2 * kLB + 1) & ~1));   // ready, done_rank
-    T *sold = reinterpret_cast<T *>(smem + (size_t)(RING + 2) * 8 + 8 * ((a.nstage + 2 * kLB + 1) & ~1) + 16);
-    const int SB = a.sbuf;   // S_old entries (power of two), indexed by rank
-    int *stag = reinterpret_cast<int *>(sold + SB);   // rank whose S_old is in the slot
-    // f output buffer (fresh warp -> writer warp): value and user id per rank
-    constexpr int FB = 1024;
-    T *fbuf = reinterpret_cast<T *>(stag + SB);
-    int *fusr = reinterpret_cast<int *>(fbuf + FB);
-    unsigned char *stage0 = reinterpret_cast<unsigned char *>(fusr + FB);
-    const unsigned stage_base = smem_u32(stage0);
-    const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
-    const unsigned sbytes = dbytes + gbytes + ubytes;
-    const int b = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
-    const int32_t nchunks = (int32_t)(a.npad >> a.lg_ch);
-    const unsigned ns = (unsigned)a.nstage;
-
-    for (int i = tid; i < SB; i += blockDim.x) stag[i] = -1;
-    if (tid == 0) {
-        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)RING * 8), "l"(0ull) : "memory");
-        for (int s2 = 0; s2 < a.nstage; s2++) mbar_init(&bars[s2], 1);
-        for (int s2 = 0; s2 < 2 * kLB; s2++) mbar_init(&lvlbar[s2], 1);
-        asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
-                     : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto wait_bar = [&](u64 *bar, int32_t Ld) {   // phase of level Ld complete
-        if (Ld < 0) return;
-        mbar_wait(&bar[Ld & (kLB - 1)], (unsigned)((Ld / kLB) & 1));
-    };
-    auto stage_row = [&](int32_t e, unsigned &st, unsigned &off) {
-        st = stage_base + ((unsigned)(e >> a.lg_ch) % ns) * sbytes;
-        off = (unsigned)(e & (ch - 1));
-    };
-
-    if (warp == kNH + 1) {
-        // ------------------------------------------------------ producer --
-        if (lane == 0) {
-            auto issue = [&](int32_t c) {
-                const int s2 = (int)((unsigned)c % ns);
-                unsigned char *st = stage0 + (size_t)s2 * sbytes;
-                const size_t r0 = (size_t)c << a.lg_ch;
-                mbar_expect_tx(&bars[s2], sbytes);
-                bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s2]);
-                bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s2]);
-                bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s2]);
-            };
-            int32_t issued = 0, arrived = 0;
-            for (; issued < nchunks && issued < a.nstage; issued++) issue(issued);
-            while (arrived < nchunks) {
-                mbar_wait(&bars[(unsigned)arrived % ns], ((unsigned)arrived / ns) & 1u);
-                arrived++;
-                df_rel(ctrl, arrived << a.lg_ch);
-                while (issued < nchunks) {
-                    const int32_t done = df_acq(ctrl + 4);
-                    if (((int64_t)(issued - a.nstage + 1) << a.lg_ch) > done) {
-                        if (arrived < issued) break;
-                        __nanosleep(64);
-                        continue;
-                    }
-                    issue(issued);
-                    issued++;
-                }
-            }
-        }
-        return;
-    }
-
-    if (warp == kNH + 2) {
-        // -------------------------------------------------------- writer --
-        // drains fbuf: ranks < done_rank (published with release by the
-        // fresh warp) are final; publishes drained (ctrl + 8) for slot reuse
-        T *f = reinterpret_cast<T *>(a.f);
-        int32_t w = 0;
-        while (w < a.n) {
-            const int32_t done = df_acq(ctrl + 4);
-            if (done <= w) { __nanosleep(32); continue; }
-            for (int32_t r = w + lane; r < done; r += 32) {
-                const int i = r & (FB - 1);
-                f[(size_t)fusr[i] * a.B + b] = fbuf[i];
-            }
-            __syncwarp();
-            w = done;
-            if (lane == 0) df_rel(ctrl + 8, w);
-        }
-        return;
-    }
-
-    if (warp >= 1) {
-        // ------------------------------------------------------- helpers --
-        const int h = warp - 1;
-        int32_t staged = 0;
-        for (int32_t L = h; L < a.ell; L += kNH) {
-            const int32_t lo = a.lvl_ptr[L], hi = a.lvl_ptr[L + 1];
-            while (staged < hi) staged = df_acq(ctrl);
-            // far deps: levels <= L-7 done.  This also frees the S_old slots
-            // this level reuses: SB >= (kMid + 4) * max level width, so the
-            // previous occupant of slot e & (SB-1) lies in a level <= L-8.
-            wait_bar(lvlbar, L - kMid - 1);
-            T sf[4];
-            unsigned rows[4];
-            const int np = min((hi - lo + 31) >> 5, 4);
-#pragma unroll
-            for (int p = 0; p < 4; p++) {
-                if (p < np) {
-                    const int32_t e = lo + 32 * p + lane, ee = e < hi ? e : lo + 32 * p;
-                    unsigned st, off;
-                    stage_row(ee, st, off);
-                    rows[p] = st + off * (unsigned)a.kp * 2;
-                    sf[p] = df_sum<T, FE>(ring_base, rows[p] + 2 * (NN + NM));
-                }
-            }
-            wait_bar(lvlbar, L - kNear - 1);
-#pragma unroll
-            for (int p = 0; p < 4; p++) {
-                if (p < np) {
-                    const int32_t e = lo + 32 * p + lane;
-                    const unsigned cn = (lds32u(rows[p] + 2 * (NN + NM + FE)) >> 16) >> 8;
-                    uint4 mw[NM / 8];
-#pragma unroll
-                    for (int q = 0; q < NM / 8; q++) mw[q] = df_lds128(rows[p] + 2 * NN + 16 * q);
-                    const T v = sf[p] + df_sum_wc<T, NM>(ring_base, mw, (int)cn);
-                    if (e < hi) {
-                        sold[e & (SB - 1)] = v;
-                        df_rel(smem_u32(&stag[e & (SB - 1)]), e);   // value, then tag (release)
-                    }
-                }
-            }
-            for (int32_t base = lo + 128; base < hi; base += 32) {   // levels wider than 128: serial
-                const int32_t e = base + lane, ee = e < hi ? e : base;
-                unsigned st, off;
-                stage_row(ee, st, off);
-                const unsigned row = st + off * (unsigned)a.kp * 2;
-                const T v = df_sum<T, FE>(ring_base, row + 2 * (NN + NM)) + df_sum<T, NM>(ring_base, row + 2 * NN);
-                if (e < hi) {
-                    sold[e & (SB - 1)] = v;
-                    df_rel(smem_u32(&stag[e & (SB - 1)]), e);
-                }
-            }
-        }
-        return;
-    }
-
-    // ---------------------------------------------------------- fresh warp --
-    // Level L's first pass uses row data loaded while level L-1's loads were
-    // in flight; S_old(x) is taken when its tag shows x (written by a helper
-    // with release semantics), so nothing but shared-memory loads, adds, the
-    // ring store and __syncwarp sit between two levels.
-    T *f = reinterpret_cast<T *>(a.f);
-    int32_t staged = 0;
-    int32_t cb = 0;
-    int32_t clo = a.lvl_ptr[min(lane, a.ell)], cnx = a.lvl_ptr[min(31 + lane, a.ell)];
-    auto bounds = [&](int32_t L, int32_t &lo, int32_t &hi) {
-        if (L >= a.ell) { lo = hi = a.n; return; }
-        if (L - cb >= 31) {
-            cb += 31;
-            clo = cnx;
-            cnx = a.lvl_ptr[min(cb + 31 + lane, a.ell)];
-        }
-        lo = __shfl_sync(0xffffffffu, clo, L - cb);
-        hi = __shfl_sync(0xffffffffu, clo, L - cb + 1);
-    };
-    struct Row { unsigned pc; uint4 nw[NN / 8]; T g; int32_t u; T so; };
-    auto load_row = [&](int32_t e, int32_t hi_, Row &R) {
-        const int32_t ee = e < hi_ ? e : hi_ - 1;
-        unsigned st, off;
-        stage_row(ee, st, off);
-        const unsigned row = st + off * (unsigned)a.kp * 2;
-        R.pc = lds32u(row + 2 * (NN + NM + FE));
-#pragma unroll
-        for (int q = 0; q < NN / 8; q++) R.nw[q] = df_lds128(row + 16 * q);
-        R.g = bits_to<T>(df_lds64(st + dbytes + off * 8));
-        R.u = e < hi_ ? (int32_t)lds32u(st + dbytes + gbytes + off * 4) : -1;
-        const unsigned ta = smem_u32(&stag[ee & (SB - 1)]);
-        while (df_acq(ta) != ee) {
-        }
-        R.so = sold[ee & (SB - 1)];
-    };
-    int32_t lo, hi;
-    int32_t drained = 0;
-    bounds(0, lo, hi);
-    Row R;
-    while (staged < hi) staged = df_acq(ctrl);
-    load_row(lo + lane, hi, R);
-    for (int32_t L = 0; L < a.ell; L++) {
-        int32_t nlo, nhi;
-        bounds(L + 1, nlo, nhi);
-        // level L, first pass: issue the near loads and F(next) ...
-        const T sn = df_sum_wc<T, NN>(ring_base, R.nw, (int)(R.pc >> 16) & 0xff);
-        const T Fp = bits_to<T>(df_lds64(ring_base + (R.pc & 0xffffu)));
-        // ... and prefetch level L+1's first pass while they are in flight
-        Row Rn;
-        if (L + 1 < a.ell) {
-            while (staged < nhi) staged = df_acq(ctrl);
-            load_row(nlo + lane, nhi, Rn);
-        }
-        {
-            const T Fx = R.g - (R.so + sn);
-            if (R.u >= 0) {
-                const int e = lo + lane;
-                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
-                             "l"(df_bits<T>(Fx))
-                             : "memory");
-                fbuf[e & (FB - 1)] = Fx - Fp;
-                fusr[e & (FB - 1)] = R.u;
-            }
-        }
-        for (int32_t base = lo + 32; base < hi; base += 32) {   // further passes of a wide level
-            Row Rx;
-            load_row(base + lane, hi, Rx);
-            const T Fx = Rx.g - (Rx.so + df_sum_wc<T, NN>(ring_base, Rx.nw, (int)(Rx.pc >> 16) & 0xff));
-            const T Fq = bits_to<T>(df_lds64(ring_base + (Rx.pc & 0xffffu)));
-            if (Rx.u >= 0) {
-                const int e = base + lane;
-                asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
-                             "l"(df_bits<T>(Fx))
-                             : "memory");
-                fbuf[e & (FB - 1)] = Fx - Fq;
-                fusr[e & (FB - 1)] = Rx.u;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lvlbar[L & (kLB - 1)]))
-                         : "memory");
-            df_rel(ctrl + 4, hi);   // ranks < hi final (producer, writer)
-        }
-        R = Rn;
-        // fbuf slots of the next level must have been drained
-        if (nhi - FB > drained) {
-            while ((drained = df_acq(ctrl + 8)) < nhi - FB) {
-            }
-        }
-        lo = nlo;
-        hi = nhi;
-    }
-}
-
 // ------------------------------------------------------------- host -------
 static constexpr size_t kSmemCapDF = 227 * 1024;
-static constexpr int kNHPlan = 6;
-static size_t ringfr_plan_smem(int ring, int sbuf, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 + 1024 * 12 +
-           (size_t)nstage * ch * ((size_t)kp * 2 + 12);
-}
 
 static size_t ringdf_smem_bytes(int ring, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + kLB + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
+    return (size_t)(ring + 16) * 8 + 8 * ((nstage + kLB + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
 }
 
 void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
-                 const unsigned counts2[2], RingDFPlan &R) {
+                 const unsigned counts3[3], RingDFPlan &R) {
     R.ok = false;
-    if (n <= 0 || k > 256 || counts2[0] > 16 || counts2[1] > 32) return;
-    R.nn = counts2[0] <= 8 ? 8 : 16;
-    R.nm = counts2[1] <= 16 ? 16 : 32;
-    R.fe = k <= 64 ? 64 : k <= 128 ? 128 : 256;
-    int32_t kp = R.nn + R.nm + R.fe + 8;   // + next slot, counts, padding
-    if ((kp / 8) % 2 == 0) kp += 8;
-    const int64_t ahead = (int64_t)(8 + kMid + 4) * max_level_width;   // up to 8 consumer warps
+    if (n <= 0 || k > 256 || counts3[0] > 16 || counts3[1] > 32 || counts3[2] > 31 * 16) return;
+    R.nn = counts3[0] <= 4 ? 4 : counts3[0] <= 8 ? 8 : 16;
+    R.nm = counts3[1] <= 16 ? 16 : 32;
+    R.fe = std::max(16, (int)(counts3[2] + 15) / 16 * 16);   // longest bank-coloured far group
+    int32_t kp = df_off_far(R.nm, R.nn) / 2 + R.fe;         // 16-byte rows
+    if ((kp / 8) % 2 == 0) kp += 8;                         // odd multiple of 16 bytes: rows spread banks
+    const int64_t ahead = (int64_t)(kNWC + kMid + 4) * max_level_width;
     int64_t ring = 32;
     while (ring < (int64_t)reach + ahead + 1) ring <<= 1;
-    if (ring > 4096) return;   // rows hold byte offsets: (RING + 1) * 8 must fit in 16 bits
+    if (ring > 4096) return;   // rows hold byte offsets: (RING + 16) * 8 must fit in 16 bits
     // the fewest stages of the largest chunk that hold 9 levels and fit
     for (int ch : {256, 128, 64, 32}) {
         for (int nstage = 2; nstage <= 8; nstage++) {
-            if ((int64_t)(nstage - 1) * ch < (int64_t)(8 + 1) * max_level_width) continue;
+            if ((int64_t)(nstage - 1) * ch < (int64_t)(kNWC + 1) * max_level_width) continue;
             if (ringdf_smem_bytes((int)ring, kp, ch, nstage) > kSmemCapDF) break;
-            {
-                R.ok = true;
-                R.kp = kp;
-                R.ring = (int32_t)ring;
-                R.ch = ch;
-                R.nstage = nstage;
-                R.npad = ((int64_t)n + ch - 1) / ch * ch;
-                R.nwc = 8;
-                // RINGFR: S_old buffer for the helpers' lead (kNH levels + slack)
-                int64_t sb = 64;
-                while (sb < (int64_t)(kNHPlan + 4) * max_level_width + 64) sb <<= 1;
-                R.sbuf = (int32_t)sb;
-                R.fr_ok = ringfr_plan_smem((int)ring, (int)sb, kp, ch, nstage) <= kSmemCapDF;
-                return;
-            }
+            R.ok = true;
+            R.kp = kp;
+            R.ring = (int32_t)ring;
+            R.ch = ch;
+            R.nstage = nstage;
+            R.npad = ((int64_t)n + ch - 1) / ch * ch;
+            R.nwc = kNWC;
+            return;
         }
     }
 }
 
+static size_t build_smem(int k, int kp) { return 2048 + (size_t)64 * (k + 1) * 2 + (size_t)32 * kp * 2 + 2 * 4096 * 2; }
+
 cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int32_t *slot_rank,
-                             unsigned *out2, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(out2, 0, 2 * sizeof(unsigned), s);
+                             unsigned *out3, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(unsigned), s);
     if (e != cudaSuccess || P.n == 0) return e;
-    k_df_counts<<<(P.n + 255) / 256, 256, 0, s>>>(P.M, P.n, P.k, P.chain, level, slot_rank, out2);
+    k_df_counts<<<(P.n + 255) / 256, 256, 0, s>>>(P.M, P.n, P.k, P.chain, level, slot_rank, out3);
+    launches_add(1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (P.k > 256 || P.ell <= 0) return cudaSuccess;   // no RINGDF plan (ringdf_plan)
+    const size_t smem = build_smem(P.k, 0);
+    e = cudaFuncSetAttribute(k_build_ringdf<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_build_ringdf<false><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, 0, 0, 0, 0, 4096, P.chain,
+                                                          P.slot, slot_rank, level, nullptr, out3 + 2);
     launches_add(1);
     return cudaGetLastError();
 }
@@ -805,58 +728,15 @@ cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int3
 cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *level,
                                 const int32_t *slot_rank, cudaStream_t s) {
     if (P.n == 0) return cudaSuccess;
-    const size_t smem = (size_t)64 * (P.k + 1) * 2 + (size_t)32 * R.kp * 2;
-    cudaError_t e = cudaFuncSetAttribute(k_build_ringdf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = build_smem(P.k, R.kp);
+    cudaError_t e = cudaFuncSetAttribute(k_build_ringdf<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_build_ringdf<<<(unsigned)(R.npad / 32), 256, smem, s>>>(P.M, P.n, P.k, R.kp, R.nn, R.nm, R.fe,
-                                                              R.ring, P.chain, P.slot, slot_rank,
-                                                              level, R.D);
+    k_build_ringdf<true><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, R.kp, R.nn, R.nm, R.fe,
+                                                         R.ring, P.chain, P.slot, slot_rank, level, R.D,
+                                                         nullptr);
     launches_add(1);
     return cudaGetLastError();
-}
-
-static constexpr int kNH = 6;   // RINGFR helper warps
-
-static size_t ringfr_smem_bytes(int ring, int sbuf, int kp, int ch, int nstage) {
-    return (size_t)(ring + 2) * 8 + 8 * ((nstage + 2 * kLB + 1) & ~1) + 16 + (size_t)sbuf * 12 + 1024 * 12 +
-           (size_t)nstage * ch * ((size_t)kp * 2 + 12);
-}
-
-cudaError_t launch_moebius_ringfr(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t B, cudaStream_t s) {
-    if (P.n == 0) return cudaSuccess;
-    RDFArgs a{};
-    a.D = R.D;
-    a.gP = gP;
-    a.ru = ru_pad;
-    a.lvl_ptr = P.lvl_ptr;
-    a.f = f;
-    a.npad = R.npad;
-    a.n = P.n;
-    a.kp = R.kp;
-    a.ell = P.ell;
-    a.B = (int32_t)B;
-    a.ring_mask = R.ring - 1;
-    a.lg_ch = 0;
-    while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
-    a.nstage = R.nstage;
-    a.sbuf = R.sbuf;
-    const size_t smem = ringfr_smem_bytes(R.ring, R.sbuf, R.kp, R.ch, R.nstage);
-    void *fn = nullptr;
-#define RFR_FN(NN, NM, FE)                                                                     \
-    if (R.nn == NN && R.nm == NM && R.fe == FE)                                                \
-        fn = dtype == 0 ? (void *)k_moeb_ringfr<u64, NN, NM, FE, kNH> : (void *)k_moeb_ringfr<double, NN, NM, FE, kNH>;
-    RFR_FN(8, 16, 64) RFR_FN(8, 32, 64) RFR_FN(16, 16, 64) RFR_FN(16, 32, 64)
-    RFR_FN(8, 16, 128) RFR_FN(8, 32, 128) RFR_FN(16, 16, 128) RFR_FN(16, 32, 128)
-    RFR_FN(8, 16, 256) RFR_FN(8, 32, 256) RFR_FN(16, 16, 256) RFR_FN(16, 32, 256)
-#undef RFR_FN
-    if (!fn || !R.fr_ok) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    void *args[] = {&a};
-    launches_add(1);
-    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNH + 3)), args, smem, s);
 }
 
 cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
@@ -881,24 +761,20 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
     a.skip_far = R.skip_far;
     const size_t smem = ringdf_smem_bytes(R.ring, R.kp, R.ch, R.nstage);
     void *fn = nullptr;
-#define RDF_FN(NN, NM, FE, W)                                                                  \
-    if (R.nn == NN && R.nm == NM && R.fe == FE && R.nwc == W)                                  \
-        fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE, W, true>            \
-                                  : (void *)k_moeb_ringdf<double, NN, NM, FE, W, true>)        \
-                    : (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, FE, W>                  \
-                                  : (void *)k_moeb_ringdf<double, NN, NM, FE, W>);
-#define RDF_W(NN, NM, FE) RDF_FN(NN, NM, FE, 4) RDF_FN(NN, NM, FE, 8)
-    RDF_W(8, 16, 64) RDF_W(8, 32, 64) RDF_W(16, 16, 64) RDF_W(16, 32, 64)
-    RDF_W(8, 16, 128) RDF_W(8, 32, 128) RDF_W(16, 16, 128) RDF_W(16, 32, 128)
-    RDF_W(8, 16, 256) RDF_W(8, 32, 256) RDF_W(16, 16, 256) RDF_W(16, 32, 256)
-#undef RDF_W
+#define RDF_FN(NN, NM)                                                                         \
+    if (R.nn == NN && R.nm == NM)                                                              \
+        fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM, true>                   \
+                                  : (void *)k_moeb_ringdf<double, NN, NM, true>)               \
+                    : (dtype == 0 ? (void *)k_moeb_ringdf<u64, NN, NM>                         \
+                                  : (void *)k_moeb_ringdf<double, NN, NM>);
+    RDF_FN(4, 16) RDF_FN(4, 32) RDF_FN(8, 16) RDF_FN(8, 32) RDF_FN(16, 16) RDF_FN(16, 32)
 #undef RDF_FN
     if (!fn) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     void *args[] = {&a};
     launches_add(1);
-    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (R.nwc + 1)), args, smem, s);
+    return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNWC + 1)), args, smem, s);
 }
 
 }  // namespace poset

@@ -28,7 +28,7 @@ for lpe in (1, 2, 4, 8):
     ms = prof["moebius_solve"][0] / 3
     res[f"lpe{lpe}_ms"] = ms
     res[f"lpe{lpe}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
-for kern, name in ((pz.MOEB_RINGFR, "ringfr"), (pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
+for kern, name in ((pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
     if (kern == pz.MOEB_RINGWS and not info["ringws"]) or (kern == pz.MOEB_RINGDF and not info["ringdf"] & 1) \
             or (kern == pz.MOEB_RINGFR and not info["ringdf"] & 2):
         continue
@@ -80,15 +80,6 @@ prof, _ = P.profile_read(); P.set_option("profile", 0)
 res["ring8_i64_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
 if info["ringdf"]:
     P.set_option("moebius_kernel", pz.MOEB_RINGDF)
-    for nwc in (4, 8):
-        P.set_option("ringdf_nwc", nwc)
-        P.moebius(g, out=y); torch.cuda.synchronize()
-        P.set_option("profile", 1); P.profile_read()
-        for _ in range(3):
-            P.moebius(g, out=y)
-        prof, _ = P.profile_read(); P.set_option("profile", 0)
-        res[f"ringdf_nwc{nwc}_clk"] = prof["moebius_solve"][0] / 3 * 1e-3 * 1.965e9 / info["ell"]
-    P.set_option("ringdf_nwc", 8)
     P.set_option("ring_debug", 8)
     P.moebius(g, out=y); torch.cuda.synchronize()
     d = P.debug_read()
