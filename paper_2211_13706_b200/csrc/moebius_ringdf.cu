@@ -294,7 +294,7 @@ __device__ __forceinline__ T df_sum(unsigned ring_base, unsigned row) {
             v[2 * h + 1] = bits_to<T>(df_lds64(ring_base + (ws[h] >> 16)));
         }
         return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-    }
+    } else {
 #pragma unroll
     for (int c = 0; c < E; c += 16) {
         const uint4 w0 = df_lds128(row + 2 * c), w1 = df_lds128(row + 2 * c + 16);
@@ -310,6 +310,7 @@ __device__ __forceinline__ T df_sum(unsigned ring_base, unsigned row) {
 #pragma unroll
             for (int i = 0; i < 16; i += 2 * st) v[i] += v[i + st];
         acc += v[0];
+    }
     }
     return acc;
 }
@@ -498,86 +499,90 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         const int32_t npass = (hi - lo + 31) >> 5;
         const int32_t np = min(npass, kNP);
         while (staged < hi) staged = df_acq(ctrl);
-        // per pass: row-derived data in registers (passes beyond kNP: serial below)
-        T gx[kNP], sp[kNP];
-        int32_t u[kNP];
-        unsigned rowa[kNP], pn[kNP], cnt[kNP];
-        unsigned nw[kNP][NN / 2];
-#pragma unroll
-        for (int p = 0; p < kNP; p++) {
-            if (p < np) {
-                const int32_t e = lo + 32 * p + lane;
-                const int32_t ee = e < hi ? e : lo + 32 * p;
-                const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
-                const unsigned off = (unsigned)(ee & (ch - 1));
-                rowa[p] = st + off * (unsigned)a.kp * 2;
-                gx[p] = bits_to<T>(df_lds64(st + dbytes + off * 8));
-                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + dbytes + gbytes + off * 4));
-                const unsigned pc = lds32u(rowa[p] + OFF_PN);
-                pn[p] = pc & 0xffffu;
-                cnt[p] = pc >> 16;   // near count | mid count << 5 | far chunks << 11
-                df_near_words<NN>(rowa[p] + OFF_NEAR, nw[p]);
-                u[p] = e < hi ? u[p] : -1;
-            } else {
-                gx[p] = T(0);
-                u[p] = -1;
-                rowa[p] = pn[p] = cnt[p] = 0;
-#pragma unroll
-                for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
-            }
-        }
-        wait_level(L - kMid - 1);   // far: levels <= L-7
-#pragma unroll
-        for (int p = 0; p < kNP; p++) {
-            if (p < np) {
-                // far entries in chunks of 16, to the longest row of the warp
-                const unsigned nf = (a.skip_far & 1) ? 0u : __reduce_max_sync(0xffffffffu, cnt[p] >> 11);
-                T acc = T(0);
-                for (unsigned c = 0; c < nf; c++) acc += df_sum<T, 16>(ring_base, rowa[p] + OFF_FAR + 32 * c);
-                sp[p] = acc;
-            }
-        }
-        wait_level(L - kNear - 1);  // mid: levels <= L-3
-#pragma unroll
-        for (int p = 0; p < kNP; p++) {
-            if (p < np) {
-                uint4 mw[NM / 8];
-#pragma unroll
-                for (int q = 0; q < NM / 8; q++) mw[q] = df_lds128(rowa[p] + 16 * q);
-                if (!(a.skip_far & 2)) sp[p] += df_sum_wc<T, NM>(ring_base, mw, (int)((cnt[p] >> 5) & 63u));
-            }
-        }
-        // Everything the critical path needs is formed (and pinned in
-        // registers) before the near wait: gx - (far + mid), the absolute ring
-        // addresses of the near slots (padding = the zero entry, so the loads
-        // need no predicates), the ring store address and predicate and the
-        // barrier address.  After the wait: NN loads per pass, the add tree,
-        // one subtract, a predicated store, __syncwarp and the arrive.
-        unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
-        df_pin(lvl_addr);
-        T gs[kNP], Fx[kNP];
-        unsigned na[kNP][NN], sa[kNP], stp[kNP];
-#pragma unroll
-        for (int p = 0; p < kNP; p++) {
-            gs[p] = p < np ? gx[p] - sp[p] : T(0);
-            df_pin(gs[p]);
-            sa[p] = ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u;
-            stp[p] = (p < np && u[p] >= 0) ? 1u : 0u;
-            df_pin(sa[p]);
-            df_pin(stp[p]);
-#pragma unroll
-            for (int q = 0; q < NN / 2; q++) {
-                const unsigned w = (a.skip_far & 4) ? (zero_off | (zero_off << 16)) : nw[p][q];
-                na[p][2 * q] = ring_base + (w & 0xffffu);
-                na[p][2 * q + 1] = ring_base + (w >> 16);
-                df_pin(na[p][2 * q]);
-                df_pin(na[p][2 * q + 1]);
-            }
-        }
-        // the level tail for NPX passes (NPX = 1: the common single-pass
-        // level, no code for the other passes in the critical path)
-        auto tail = [&](auto npx) {
+        // One level, NPX passes of 32 elements in registers (NPX = 1: the
+        // common single-pass level, no code for other passes; NPX = kNP:
+        // passes p < np, the rest serially after the near wait).
+        auto level = [&](auto npx) {
             constexpr int NPX = decltype(npx)::value;
+            auto act = [&](int p) { return NPX == 1 || p < np; };
+            T gx[NPX], sp[NPX];
+            int32_t u[NPX];
+            unsigned rowa[NPX], pn[NPX], cnt[NPX];
+            unsigned nw[NPX][NN / 2];
+#pragma unroll
+            for (int p = 0; p < NPX; p++) {
+                if (act(p)) {
+                    const int32_t e = lo + 32 * p + lane;
+                    const int32_t ee = e < hi ? e : lo + 32 * p;
+                    const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
+                    const unsigned off = (unsigned)(ee & (ch - 1));
+                    rowa[p] = st + off * (unsigned)a.kp * 2;
+                    gx[p] = bits_to<T>(df_lds64(st + dbytes + off * 8));
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + dbytes + gbytes + off * 4));
+                    const unsigned pc = lds32u(rowa[p] + OFF_PN);
+                    pn[p] = pc & 0xffffu;
+                    cnt[p] = pc >> 16;   // near count | mid count << 5 | far chunks << 11
+                    df_near_words<NN>(rowa[p] + OFF_NEAR, nw[p]);
+                    u[p] = e < hi ? u[p] : -1;
+                } else {
+                    gx[p] = T(0);
+                    u[p] = -1;
+                    rowa[p] = pn[p] = cnt[p] = 0;
+#pragma unroll
+                    for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
+                }
+            }
+            wait_level(L - kMid - 1);   // far: levels <= L-7
+#pragma unroll
+            for (int p = 0; p < NPX; p++) {
+                if (act(p)) {
+                    // far entries in chunks of 16, to the longest row of the warp
+                    const unsigned nf = (a.skip_far & 1) ? 0u : __reduce_max_sync(0xffffffffu, cnt[p] >> 11);
+                    T acc = T(0);
+                    for (unsigned c = 0; c < nf; c++) acc += df_sum<T, 16>(ring_base, rowa[p] + OFF_FAR + 32 * c);
+                    sp[p] = acc;
+                }
+            }
+            wait_level(L - kNear - 1);  // mid: levels <= L-3
+#pragma unroll
+            for (int p = 0; p < NPX; p++) {
+                if (act(p)) {
+                    // mid entries in chunks of 8 (zero-entry padded), to the warp's longest
+                    const unsigned nm8 =
+                        (a.skip_far & 2) ? 0u : (__reduce_max_sync(0xffffffffu, (cnt[p] >> 5) & 63u) + 7) >> 3;
+                    T acc = T(0);
+                    for (unsigned c = 0; c < nm8; c++) acc += df_sum<T, 8>(ring_base, rowa[p] + 16 * c);
+                    sp[p] += acc;
+                }
+            }
+            // Everything the critical path needs is formed (and pinned in
+            // registers) before the near wait: gx - (far + mid), the absolute
+            // ring addresses of the near slots (padding = the zero entry, so
+            // the loads need no predicates), the ring store address and
+            // predicate and the barrier address.  After the wait: NN loads per
+            // pass, the add tree, one subtract, a predicated store,
+            // __syncwarp and the arrive.
+            unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
+            df_pin(lvl_addr);
+            T gs[NPX], Fx[NPX];
+            unsigned na[NPX][NN], sa[NPX], stp[NPX];
+#pragma unroll
+            for (int p = 0; p < NPX; p++) {
+                gs[p] = act(p) ? gx[p] - sp[p] : T(0);
+                df_pin(gs[p]);
+                sa[p] = ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u;
+                stp[p] = (act(p) && u[p] >= 0) ? 1u : 0u;
+                df_pin(sa[p]);
+                df_pin(stp[p]);
+#pragma unroll
+                for (int q = 0; q < NN / 2; q++) {
+                    const unsigned w = (a.skip_far & 4) ? (zero_off | (zero_off << 16)) : nw[p][q];
+                    na[p][2 * q] = ring_base + (w & 0xffffu);
+                    na[p][2 * q + 1] = ring_base + (w >> 16);
+                    df_pin(na[p][2 * q]);
+                    df_pin(na[p][2 * q + 1]);
+                }
+            }
             long long t_wait = 0;
             if (PROF) t_wait = clock64();
             wait_level(L - 1);          // near: the critical path
@@ -651,16 +656,16 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 prof[6] += np;
                 prof_last = (unsigned long long)t;
             }
+            // f(x) = F(x) - F(next below on the chain), after the publish, off
+            // the critical path (the pn slot stays live: RING >= reach + 18 wmax)
+#pragma unroll
+            for (int p = 0; p < NPX; p++)
+                if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
         };
         if (np <= 1)
-            tail(std::integral_constant<int, 1>{});
+            level(std::integral_constant<int, 1>{});
         else
-            tail(std::integral_constant<int, kNP>{});
-        // f(x) = F(x) - F(next below on the chain), after the publish, off the
-        // critical path (the pn slot stays live: RING >= reach + 18 wmax)
-#pragma unroll
-        for (int p = 0; p < kNP; p++)
-            if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
+            level(std::integral_constant<int, kNP>{});
     }
     if (PROF) {
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kNWC));
