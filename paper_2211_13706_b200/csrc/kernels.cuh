@@ -130,7 +130,8 @@ cudaError_t launch_moebius_ringws(const DevPoset &P, const RingWSPlan &R, const 
 struct RingDFPlan {
     bool ok = false;
     int32_t nn = 0, nm = 0, fe = 0;   // near / mid / far row entries (far: bank-coloured, /16)
-    int32_t kp = 0, ring = 0, ch = 0, nstage = 0;
+    int32_t kp = 0, ring = 0, ch = 0, nstage = 0;   // kp = kpn + kpf
+    int32_t kpn = 0, kpf = 0;         // near-table / far-table row entries (D = near | far tables)
     int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only

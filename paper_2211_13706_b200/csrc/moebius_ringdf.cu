@@ -92,10 +92,11 @@ __host__ __device__ constexpr int df_off_far(int nm, int nn) { return (2 * (nm +
 template <bool WRITE>
 __global__ void __launch_bounds__(256) k_build_ringdf(
     const int32_t *__restrict__ M, int32_t n, int32_t k, const int32_t *__restrict__ lvl_ptr,
-    int32_t kp, int32_t nn, int32_t nm, int32_t fe, int32_t ring,
+    int32_t kpn, int32_t kpf, int32_t nn, int32_t nm, int32_t fe, int32_t ring,
     const int32_t *__restrict__ chain, const int32_t *__restrict__ slot,
     const int32_t *__restrict__ slot_rank, const int32_t *__restrict__ level,
-    uint16_t *__restrict__ D, unsigned *__restrict__ jmax) {
+    uint16_t *__restrict__ Dn, uint16_t *__restrict__ Df, unsigned *__restrict__ jmax) {
+    const int kp = kpn + kpf;   // tile rows: near table row | far table row
     extern __shared__ __align__(16) unsigned char dsm[];
     const int ks = k + 1;
     unsigned long long *posmask = reinterpret_cast<unsigned long long *>(dsm);   // [2][16][4]
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(256) k_build_ringdf(
     const int lo = lvl_ptr[L], hi = lvl_ptr[L + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int mask = ring - 1;
-    const int ofar = df_off_far(nm, nn) / 2;
+    const int ofar = kpn;
     for (int r0 = lo; r0 < hi; r0 += 32) {
         const int nr = min(32, hi - r0);
         const int r = r0 + lane;
@@ -210,15 +211,17 @@ __global__ void __launch_bounds__(256) k_build_ringdf(
                 for (int j = 0; j < k; j++) { nnear += cls[lane * ks + j] == 0; nmid += cls[lane * ks + j] == 1; }
                 outr[lane * kp + nm + nn + 1] =
                     (uint16_t)(min(nnear, nn) | (min(nmid, nm) << 5) | (jh[lane >> 4] << 11));
+                outr[lane * kp + ofar + fe] = (uint16_t)jh[lane >> 4];   // far chunks, in the far table
             }
             __syncthreads();
             // ring slots -> byte offsets (slot * 8; (RING + 16) * 8 <= 65536 by
-            // the plan), except the counts word
-            const int64_t base = (int64_t)r0 * kp;
+            // the plan), except the two count words
             for (int t = threadIdx.x; t < nr * kp; t += blockDim.x) {
-                const int j = t % kp;
+                const int j = t % kp, rr = r0 + t / kp;
                 const uint16_t v = outr[t];
-                D[base + t] = j == nm + nn + 1 ? v : (uint16_t)(v * 8);
+                const uint16_t o = (j == nm + nn + 1 || j == ofar + fe) ? v : (uint16_t)(v * 8);
+                if (j < kpn) Dn[(int64_t)rr * kpn + j] = o;
+                else Df[(int64_t)rr * kpf + (j - kpn)] = o;
             }
         }
         __syncthreads();
@@ -227,13 +230,14 @@ __global__ void __launch_bounds__(256) k_build_ringdf(
 
 // ------------------------------------------------------------ kernel ------
 struct RDFArgs {
-    const uint16_t *D;          // [npad][kp]
+    const uint16_t *Dn;         // [npad][kpn] mid | near | pn | counts
+    const uint16_t *Df;         // [npad][kpf] far (bank-coloured) | far chunks
     const void *gP;             // [B][npad]
     const int32_t *ru;          // [npad]
     const int32_t *lvl_ptr;     // [ell + 1]
     void *f;                    // [n][B]
     int64_t npad;
-    int32_t n, kp, ell, B;
+    int32_t n, kpn, kpf, ell, B;
     int32_t ring_mask;
     int32_t lg_ch, nstage;
     int32_t skip_far;           // timing experiment only (results invalid): bit 0 far, bit 1 mid,
@@ -396,8 +400,8 @@ __device__ __forceinline__ T df_sum_u16(unsigned ring_base, unsigned row) {
 
 template <typename T, int NN, int NM, bool PROF = false>
 __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
-    // row layout, byte offsets (rows are [kp] uint16): mid | near | pn, counts | far
-    constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN), OFF_FAR = df_off_far(NM, NN);
+    // near-table row (byte offsets): mid | near | pn, counts; the far row is separate
+    constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN);
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
     const int ch = 1 << a.lg_ch;
@@ -406,7 +410,9 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
     const unsigned ctrl = smem_u32(bars + ((a.nstage + kLB + 1) & ~1));   // ready, done_rank
     unsigned char *stage0 = smem + (size_t)(RING + 16) * 8 + 8 * ((a.nstage + kLB + 1) & ~1) + 16;
     const unsigned stage_base = smem_u32(stage0);
-    const unsigned dbytes = (unsigned)ch * a.kp * 2, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
+    // stage: near rows | far rows | g | user ids
+    const unsigned nbytes = (unsigned)ch * a.kpn * 2, fbytes = (unsigned)ch * a.kpf * 2;
+    const unsigned dbytes = nbytes + fbytes, gbytes = (unsigned)ch * 8, ubytes = (unsigned)ch * 4;
     const unsigned sbytes = dbytes + gbytes + ubytes;
     const int b = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -433,7 +439,8 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 unsigned char *st = stage0 + (size_t)s * sbytes;
                 const size_t r0 = (size_t)c << a.lg_ch;
                 mbar_expect_tx(&bars[s], sbytes);
-                bulk_g2s(st, a.D + r0 * a.kp, dbytes, &bars[s]);
+                bulk_g2s(st, a.Dn + r0 * a.kpn, nbytes, &bars[s]);
+                bulk_g2s(st + nbytes, a.Df + r0 * a.kpf, fbytes, &bars[s]);
                 bulk_g2s(st + dbytes, gcol + r0, gbytes, &bars[s]);
                 bulk_g2s(st + dbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
             };
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             auto act = [&](int p) { return NPX == 1 || p < np; };
             T gx[NPX], sp[NPX];
             int32_t u[NPX];
-            unsigned rowa[NPX], pn[NPX], cnt[NPX];
+            unsigned rowa[NPX], rowf[NPX], pn[NPX], cnt[NPX];
             unsigned nw[NPX][NN / 2];
 #pragma unroll
             for (int p = 0; p < NPX; p++) {
@@ -516,7 +523,8 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                     const int32_t ee = e < hi ? e : lo + 32 * p;
                     const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
                     const unsigned off = (unsigned)(ee & (ch - 1));
-                    rowa[p] = st + off * (unsigned)a.kp * 2;
+                    rowa[p] = st + off * (unsigned)a.kpn * 2;
+                    rowf[p] = st + nbytes + off * (unsigned)a.kpf * 2;
                     gx[p] = bits_to<T>(df_lds64(st + dbytes + off * 8));
                     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + dbytes + gbytes + off * 4));
                     const unsigned pc = lds32u(rowa[p] + OFF_PN);
@@ -527,7 +535,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                 } else {
                     gx[p] = T(0);
                     u[p] = -1;
-                    rowa[p] = pn[p] = cnt[p] = 0;
+                    rowa[p] = rowf[p] = pn[p] = cnt[p] = 0;
 #pragma unroll
                     for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
                 }
@@ -539,7 +547,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                     // far entries in chunks of 16, to the longest row of the warp
                     const unsigned nf = (a.skip_far & 1) ? 0u : __reduce_max_sync(0xffffffffu, cnt[p] >> 11);
                     T acc = T(0);
-                    for (unsigned c = 0; c < nf; c++) acc += df_sum<T, 16>(ring_base, rowa[p] + OFF_FAR + 32 * c);
+                    for (unsigned c = 0; c < nf; c++) acc += df_sum<T, 16>(ring_base, rowf[p] + 32 * c);
                     sp[p] = acc;
                 }
             }
@@ -620,14 +628,15 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
                     const int32_t ee = e < hi ? e : base;
                     const unsigned st = stage_base + ((unsigned)(ee >> a.lg_ch) % ns) * sbytes;
                     const unsigned off = (unsigned)(ee & (ch - 1));
-                    const unsigned row = st + off * (unsigned)a.kp * 2;
+                    const unsigned row = st + off * (unsigned)a.kpn * 2;
+                    const unsigned row_f = st + nbytes + off * (unsigned)a.kpf * 2;
                     const T g1 = bits_to<T>(df_lds64(st + dbytes + off * 8));
                     int32_t u1;
                     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + dbytes + gbytes + off * 4));
                     const unsigned pc1 = lds32u(row + OFF_PN);
                     const unsigned p16 = pc1 & 0xffffu;
                     T s1 = df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
-                    for (unsigned c = 0; c < (pc1 >> 27); c++) s1 += df_sum<T, 16>(ring_base, row + OFF_FAR + 32 * c);
+                    for (unsigned c = 0; c < (pc1 >> 27); c++) s1 += df_sum<T, 16>(ring_base, row_f + 32 * c);
                     const T F1 = g1 - s1;
                     if (e < hi) {
                         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(e & a.ring_mask) * 8),
@@ -677,9 +686,10 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
 // ------------------------------------------------------------- host -------
 static constexpr size_t kSmemCapDF = 227 * 1024;
 
-static size_t ringdf_smem_bytes(int ring, int kp, int ch, int nstage) {
+static size_t ringdf_smem_bytes(int ring, int kp, int ch, int nstage) {   // kp = kpn + kpf
     return (size_t)(ring + 16) * 8 + 8 * ((nstage + kLB + 1) & ~1) + 16 + (size_t)nstage * ch * ((size_t)kp * 2 + 12);
 }
+static int32_t odd16(int32_t e) { return (e / 8) % 2 == 0 ? e + 8 : e; }   // rows of 16 * odd bytes
 
 void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
                  const unsigned counts3[3], RingDFPlan &R) {
@@ -688,8 +698,9 @@ void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
     R.nn = counts3[0] <= 4 ? 4 : counts3[0] <= 8 ? 8 : 16;
     R.nm = counts3[1] <= 16 ? 16 : 32;
     R.fe = std::max(16, (int)(counts3[2] + 15) / 16 * 16);   // longest bank-coloured far group
-    int32_t kp = df_off_far(R.nm, R.nn) / 2 + R.fe;         // 16-byte rows
-    if ((kp / 8) % 2 == 0) kp += 8;                         // odd multiple of 16 bytes: rows spread banks
+    R.kpn = odd16(df_off_far(R.nm, R.nn) / 2);   // near-table rows (16 * odd bytes: rows spread banks)
+    R.kpf = odd16(R.fe + 8);                      // far rows + chunk count
+    const int32_t kp = R.kpn + R.kpf;
     const int64_t ahead = (int64_t)(kNWC + kMid + 4) * max_level_width;
     int64_t ring = 32;
     while (ring < (int64_t)reach + ahead + 1) ring <<= 1;
@@ -724,8 +735,9 @@ cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int3
     const size_t smem = build_smem(P.k, 0);
     e = cudaFuncSetAttribute(k_build_ringdf<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_build_ringdf<false><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, 0, 0, 0, 0, 4096, P.chain,
-                                                          P.slot, slot_rank, level, nullptr, out3 + 2);
+    k_build_ringdf<false><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, 0, 0, 0, 0, 0, 4096,
+                                                          P.chain, P.slot, slot_rank, level, nullptr, nullptr,
+                                                          out3 + 2);
     launches_add(1);
     return cudaGetLastError();
 }
@@ -737,9 +749,9 @@ cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const in
     cudaError_t e = cudaFuncSetAttribute(k_build_ringdf<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_build_ringdf<true><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, R.kp, R.nn, R.nm, R.fe,
-                                                         R.ring, P.chain, P.slot, slot_rank, level, R.D,
-                                                         nullptr);
+    k_build_ringdf<true><<<(unsigned)P.ell, 256, smem, s>>>(P.M, P.n, P.k, P.lvl_ptr, R.kpn, R.kpf, R.nn, R.nm,
+                                                         R.fe, R.ring, P.chain, P.slot, slot_rank, level, R.D,
+                                                         R.D + R.npad * R.kpn, nullptr);
     launches_add(1);
     return cudaGetLastError();
 }
@@ -748,14 +760,16 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
                                   int dtype, const void *gP, void *f, int64_t B, cudaStream_t s) {
     if (P.n == 0) return cudaSuccess;
     RDFArgs a;
-    a.D = R.D;
+    a.Dn = R.D;
+    a.Df = R.D + R.npad * R.kpn;
     a.gP = gP;
     a.ru = ru_pad;
     a.lvl_ptr = P.lvl_ptr;
     a.f = f;
     a.npad = R.npad;
     a.n = P.n;
-    a.kp = R.kp;
+    a.kpn = R.kpn;
+    a.kpf = R.kpf;
     a.ell = P.ell;
     a.B = (int32_t)B;
     a.ring_mask = R.ring - 1;
