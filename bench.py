@@ -38,7 +38,7 @@ PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
                 "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
                 "chain_diff": "k_chain_diff"}
-MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf", "ringfr"]
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf", "ringcl"]
 
 
 def parse():

@@ -82,9 +82,9 @@ typedef enum {
                                  publish level completion through mbarriers; far / mid
                                  dependencies are summed levels ahead, near ones on the
                                  critical path                                               */
-    POSET_MOEB_RINGFR = 8     /* experimental (slower than RINGDF on C5w, never chosen by AUTO):
-                                 RINGDF tables, critical path kept in one "fresh" warp,
-                                 far + mid sums by helper warps             */
+    POSET_MOEB_RINGCL = 8     /* RINGDF over a CTA pair (cluster of 2) per column: the second
+                                 SM sums the far dependencies and returns them through
+                                 distributed shared memory                  */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -111,7 +111,7 @@ typedef struct {
     int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
     int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
-    int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGFR available       */
+    int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGCL available       */
 } poset_info;
 
 /*

@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = ["Poset", "PosetError", "analyze", "lib", "MOEB_AUTO", "MOEB_LEVEL", "MOEB_GRID", "MOEB_WARP",
            "MOEB_RING", "MOEB_CSR", "MOEB_RINGWS", "MOEB_RINGDF",
-           "MOEB_RINGFR", "LIB_PATH"]
+           "MOEB_RINGCL", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposet.so")
 
@@ -36,7 +36,7 @@ try:
 except OSError as e:   # pragma: no cover
     raise ImportError(f"cannot load {LIB_PATH}: {e} (there is no CPU fallback)") from e
 
-MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS, MOEB_RINGDF, MOEB_RINGFR = (
+MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS, MOEB_RINGDF, MOEB_RINGCL = (
     0, 1, 2, 3, 4, 5, 6, 7, 8)
 _I64, _F64 = 0, 1
 _vp = ctypes.c_void_p

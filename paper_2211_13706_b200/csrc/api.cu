@@ -232,11 +232,12 @@ static poset_status finish_setup(poset_s *h) {
                    (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0) +
                    (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
-    I.ringdf = h->rdf.ok ? 1 : 0;   // bit 1 (RINGFR, removed) stays clear
+    I.ringdf = h->rdf.ok ? (ringcl_fits(h->rdf) ? 3 : 1) : 0;   // bit 1: RINGCL
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
-    I.moebius_kernel = h->rdf.ok   ? MOEB_RINGDF
+    I.moebius_kernel = ringcl_fits(h->rdf) ? MOEB_RINGCL   // (for a batch that fits 2 SMs per column)
+                       : h->rdf.ok   ? MOEB_RINGDF
                        : h->rws.ok   ? MOEB_RINGWS
                        : h->ring.ok  ? MOEB_RING
                        : h->csr.ok ? MOEB_CSR
@@ -399,7 +400,9 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
     poset_status st = ensure_F(h, B, s);
     if (st) return st;
     DevPoset P = h->dev();
+    // AUTO: the CTA-pair schedule when two SMs per column fit in one wave
     int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
+                : (ringcl_fits(h->rdf) && 2 * B <= h->num_sms) ? MOEB_RINGCL
                 : h->rdf.ok  ? MOEB_RINGDF
                 : h->rws.ok  ? MOEB_RINGWS
                 : h->ring.ok ? MOEB_RING
@@ -414,11 +417,11 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
-    if (which == MOEB_RINGFR)
-        return fail(POSET_EINVAL, "poset_moebius: the RINGFR schedule was removed (slower than RINGDF); use AUTO");
-    if (which == MOEB_RINGDF) {
+    if (which == MOEB_RINGDF || which == MOEB_RINGCL) {
         if (!h->rdf.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
+        if (which == MOEB_RINGCL && !ringcl_fits(h->rdf))
+            return fail(POSET_EINVAL, "poset_moebius: the RINGCL schedule does not fit this poset; use AUTO");
         st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
         if (st) return st;
         {
@@ -426,7 +429,10 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
             CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
         }
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+        if (which == MOEB_RINGCL)
+            CK(launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+        else
+            CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
         return POSET_OK;
     }
     if (which == MOEB_RINGWS) {
@@ -628,7 +634,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_RINGFR) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RINGCL) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }

@@ -55,7 +55,7 @@ cudaError_t launch_gather(const DevPoset &P, int dtype, const void *F, void *g, 
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
 enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5,
-                  MOEB_RINGWS = 6, MOEB_RINGDF = 7, MOEB_RINGFR = 8 };
+                  MOEB_RINGWS = 6, MOEB_RINGDF = 7, MOEB_RINGCL = 8 };
 int moebius_pick(const DevPoset &P, int64_t batch, int max_level_width, int num_sms);
 cudaError_t launch_moebius_solve(const DevPoset &P, const int32_t *h_lvl_ptr, int dtype,
                                  const void *g, void *F, int64_t batch, int which,
@@ -132,6 +132,9 @@ struct RingDFPlan {
     int32_t nn = 0, nm = 0, fe = 0;   // near / mid / far row entries (far: bank-coloured, /16)
     int32_t kp = 0, ring = 0, ch = 0, nstage = 0;   // kp = kpn + kpf
     int32_t kpn = 0, kpf = 0;         // near-table / far-table row entries (D = near | far tables)
+    int32_t wmax = 0;                 // widest level
+    int32_t ch_h = 0, nstage_h = 0;   // RINGCL helper staging
+    bool cl_ok = false;               // RINGCL fits shared memory
     int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only
@@ -146,6 +149,11 @@ cudaError_t launch_df_counts(const DevPoset &P, const int32_t *level, const int3
 cudaError_t launch_build_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *level,
                                 const int32_t *slot_rank, cudaStream_t s);
 cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
+                                  int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
+// RINGCL: the same tables over a CTA pair per column (far sums on the second SM)
+bool ringcl_fits(const RingDFPlan &R);
+void ringcl_plan(RingDFPlan &R);
+cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
                                   int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
 
 // ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----

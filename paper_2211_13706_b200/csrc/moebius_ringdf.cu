@@ -43,6 +43,7 @@ static constexpr int kMid = 6;     // kNear < distance <= kMid: mid; beyond: far
 static constexpr int kLB = 16;     // level-completion mbarriers (ring), > kMid + 1
 static constexpr int kNP = 3;      // passes of 32 elements kept in registers per level
 static constexpr int kNWC = 8;     // consumer warps (levels round-robin)
+static constexpr int kMaxStageCL = 32;   // RINGCL stage barriers
 
 // ------------------------------------------------------------ setup -------
 // max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
@@ -237,9 +238,10 @@ struct RDFArgs {
     const int32_t *lvl_ptr;     // [ell + 1]
     void *f;                    // [n][B]
     int64_t npad;
-    int32_t n, kpn, kpf, ell, B;
+    int32_t n, kpn, kpf, fe, ell, B;
     int32_t ring_mask;
     int32_t lg_ch, nstage;
+    int32_t lg_chh, nstage_h;   // RINGCL helper staging
     int32_t skip_far;           // timing experiment only (results invalid): bit 0 far, bit 1 mid,
                                 // bit 2 near sums skipped
     unsigned long long *dbg;    // PROF instantiation only: [0] Σ ready->publish, [1] Σ publish->ready
@@ -717,6 +719,8 @@ void ringdf_plan(int32_t n, int32_t k, int32_t max_level_width, unsigned reach,
             R.nstage = nstage;
             R.npad = ((int64_t)n + ch - 1) / ch * ch;
             R.nwc = kNWC;
+            R.wmax = max_level_width;
+            ringcl_plan(R);
             return;
         }
     }
@@ -794,6 +798,501 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
     void *args[] = {&a};
     launches_add(1);
     return cudaLaunchKernel(fn, dim3((unsigned)B), dim3(32 * (kNWC + 1)), args, smem, s);
+}
+
+// ---------------------------------------------------------------------------
+// Schedule RINGCL: RINGDF over a CTA pair (cluster of 2) per column, so that
+// a second SM's shared-memory pipe and issue slots take the far sums.
+//   owner  (cluster rank 0): the level pipeline of RINGDF -- rows (near
+//          table), mid sums, the near wait, F into its ring -- but the far
+//          sum of each element comes from the helper through DSMEM (sfar,
+//          announced on farbar[L % kLB]).  After publishing level L locally it
+//          forwards F to the helper's ring (st.shared::cluster) and arrives
+//          (release.cluster) on the helper's lvlbar[L % kLB].
+//   helper (cluster rank 1): 8 warps own levels round-robin; once the
+//          owner's levels <= L-7 have arrived (its lvlbar phases L-14 ..
+//          L-7; older ones it saw at level L-8) it sums the far entries of
+//          level L (far table, bank-coloured) and writes the sums into the
+//          owner's sfar, then arrives on the owner's farbar[L % kLB].
+// Slack: the far sum of level L is needed when level L-1 completes, i.e.
+// 6 level times after level L-7 completed -- enough for two DSMEM hops.
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cl_mapa(unsigned a, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st64(unsigned ra, u64 v) {
+    asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cl_arrive_remote(unsigned ra) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+// DSMEM store that signals its bytes on the destination CTA's mbarrier
+__device__ __forceinline__ void cl_st_async64(unsigned ra, u64 v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_expect(unsigned a, unsigned bytes) {   // the phase's single arrival
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cl_arrive_local(unsigned a) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// wait for a phase completed by st.async complete_tx bytes (the transaction
+// mechanism makes the bytes visible; CTA-scope acquire, so no L1 invalidate
+// -- a cluster-scope acquire costs a CCTL.IVALL per wait)
+__device__ __forceinline__ void cl_wait(unsigned a, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWC_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WC_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cl_wait_cta(unsigned a, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWL_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WL_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <typename T, int NN, int NM, int FEC>
+__global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
+    constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int RING = a.ring_mask + 1;
+    const unsigned crank = cl_rank(), peer = crank ^ 1u;
+    const bool owner = crank == 0;
+    // role-specific staging (the helper's warps finish out of order, so it
+    // keeps more rows in flight)
+    const int lgc = owner ? a.lg_ch : a.lg_chh;
+    const int ch = 1 << lgc;
+    const unsigned ring_base = smem_u32(smem);                         // RING + 16 entries
+    const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // RING entries (owner)
+    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(2 * RING + 16) * 8);
+    constexpr int nb = kMaxStageCL + 2 * kLB;   // stage | lvlbar | farbar
+    const unsigned lvl_u32 = smem_u32(bars + kMaxStageCL), far_u32 = lvl_u32 + kLB * 8;
+    unsigned *ctrl_p = reinterpret_cast<unsigned *>(bars + nb);   // ready | done | prog[8]
+    const unsigned ctrl = smem_u32(ctrl_p);
+    unsigned char *stage0 = reinterpret_cast<unsigned char *>(ctrl_p + 12);
+    const unsigned stage_base = smem_u32(stage0);
+    // owner stage: near rows | g | user ids;  helper stage: far rows
+    const unsigned nbytes = owner ? (unsigned)ch * a.kpn * 2 : 0u, fbytes = owner ? 0u : (unsigned)ch * a.kpf * 2;
+    const unsigned gbytes = owner ? (unsigned)ch * 8 : 0u, ubytes = owner ? (unsigned)ch * 4 : 0u;
+    const unsigned sbytes = nbytes + fbytes + gbytes + ubytes;
+    const int b = blockIdx.x >> 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
+    const int32_t nchunks = (int32_t)(a.npad >> lgc);
+    const int nstage = owner ? a.nstage : a.nstage_h;
+    const unsigned ns = (unsigned)nstage;
+    T *f = reinterpret_cast<T *>(a.f);
+    const unsigned zero_off = (unsigned)RING * 8u;
+    __shared__ long long pubt[64];   // instrumentation (a.dbg): owner publish clock per level
+
+    if (tid < 16)
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(RING + tid) * 8), "l"(0ull) : "memory");
+    if (tid == 0) {
+        for (int s = 0; s < nb; s++) mbar_init(&bars[s], 1);
+        for (int i = 0; i < 10; i++) ctrl_p[i] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl_sync();   // both CTAs' barriers initialised before any remote arrive
+
+    auto wait_lvl = [&](int32_t Ld) {   // local level completion (owner)
+        if (Ld < 0) return;
+        cl_wait_cta(lvl_u32 + (unsigned)(Ld & (kLB - 1)) * 8u, (unsigned)((Ld / kLB) & 1));
+    };
+    if (warp == kNWC) {
+        // ------------------------------------------------------ producer --
+        if (owner && lane == 0) {
+            auto issue = [&](int32_t c) {
+                const int s = (int)((unsigned)c % ns);
+                unsigned char *st = stage0 + (size_t)s * sbytes;
+                const size_t r0 = (size_t)c << lgc;
+                mbar_expect_tx(&bars[s], sbytes);
+                if (owner) {
+                    bulk_g2s(st, a.Dn + r0 * a.kpn, nbytes, &bars[s]);
+                    bulk_g2s(st + nbytes, gcol + r0, gbytes, &bars[s]);
+                    bulk_g2s(st + nbytes + gbytes, a.ru + r0, ubytes, &bars[s]);
+                } else {
+                    bulk_g2s(st, a.Df + r0 * a.kpf, fbytes, &bars[s]);
+                }
+            };
+            // consumers' progress: owner levels finish in order (done word);
+            // helper warps finish out of order (minimum of per-warp words)
+            auto progress = [&]() -> int32_t {
+                if (owner) return df_acq(ctrl + 4);
+                int32_t m = 0x7fffffff;
+                for (int w = 0; w < kNWC; w++) m = min(m, df_acq(ctrl + 8 + 4 * w));
+                return m;
+            };
+            int32_t issued = 0, arrived = 0;
+            for (; issued < nchunks && issued < nstage; issued++) issue(issued);
+            while (arrived < nchunks) {
+                mbar_wait(&bars[(unsigned)arrived % ns], ((unsigned)arrived / ns) & 1u);
+                arrived++;
+                df_rel(ctrl, arrived << lgc);
+                while (issued < nchunks) {
+                    const int32_t done = progress();
+                    if (((int64_t)(issued - nstage + 1) << lgc) > done) {
+                        if (arrived < issued) break;
+                        __nanosleep(64);
+                        continue;
+                    }
+                    issue(issued);
+                    issued++;
+                }
+            }
+        }
+    } else if (!owner) {
+        // -------------------------------------------------- helper warps --
+        // Far rows come straight from global memory into registers, issued
+        // before the wait for the owner's levels (their latency hides behind
+        // it); no staging, so no coupling between the out-of-order helper
+        // warps and a stage ring.
+        int32_t hcb = 0, hlo, hhi;   // level bounds of this warp's next 32 levels, in registers
+        hlo = a.lvl_ptr[min(warp + lane * kNWC, a.ell)];
+        hhi = a.lvl_ptr[min(warp + lane * kNWC + 1, a.ell)];
+        auto far_sum = [&](const uint4 (&w)[2 * FEC], unsigned nf) -> T {
+            T acc = T(0);
+#pragma unroll
+            for (int c = 0; c < FEC; c++) {
+                if ((unsigned)c >= nf) break;   // warp-uniform: the group's colour count
+                const unsigned ws[8] = {w[2 * c].x, w[2 * c].y, w[2 * c].z, w[2 * c].w,
+                                        w[2 * c + 1].x, w[2 * c + 1].y, w[2 * c + 1].z, w[2 * c + 1].w};
+                T v[16];
+#pragma unroll
+                for (int h = 0; h < 8; h++) {
+                    v[2 * h] = bits_to<T>(df_lds64(ring_base + (ws[h] & 0xffffu)));
+                    v[2 * h + 1] = bits_to<T>(df_lds64(ring_base + (ws[h] >> 16)));
+                }
+#pragma unroll
+                for (int st2 = 1; st2 < 16; st2 <<= 1)
+#pragma unroll
+                    for (int j = 0; j < 16; j += 2 * st2) v[j] += v[j + st2];
+                acc += v[0];
+            }
+            return acc;
+        };
+        auto load_row = [&](int32_t ee, uint4 (&w)[2 * FEC], unsigned &c16) {
+            const uint4 *rg = reinterpret_cast<const uint4 *>(a.Df + (size_t)ee * a.kpf);
+            const int nq = a.fe / 8;   // the row's 16-byte words (fe <= 16 * FEC)
+#pragma unroll
+            for (int q = 0; q < 2 * FEC; q++) w[q] = q < nq ? __ldg(rg + q) : make_uint4(0, 0, 0, 0);
+            c16 = __ldg(a.Df + (size_t)ee * a.kpf + a.fe);   // 16-entry chunks used by this row's group
+        };
+        uint4 w0[2 * FEC], wn[2 * FEC];
+        unsigned c0 = 0, cn = 0;
+        if (warp < a.ell) {
+            const int32_t lo0 = __shfl_sync(0xffffffffu, hlo, 0), hi0 = __shfl_sync(0xffffffffu, hhi, 0);
+            load_row(lo0 + lane < hi0 ? lo0 + lane : lo0, wn, cn);
+        }
+        for (int32_t L = warp, i = 0; L < a.ell; L += kNWC, i++) {
+            if (i - hcb == 32) {
+                hcb += 32;
+                hlo = a.lvl_ptr[min(warp + (hcb + lane) * kNWC, a.ell)];
+                hhi = a.lvl_ptr[min(warp + (hcb + lane) * kNWC + 1, a.ell)];
+            }
+            const int32_t lo = __shfl_sync(0xffffffffu, hlo, i - hcb), hi = __shfl_sync(0xffffffffu, hhi, i - hcb);
+            // arm this level's phase: the owner's F values of level L land here
+            // with st.async (8 bytes per element); phase L-16 is complete (this
+            // warp waited for it at level L-8)
+            if (lane == 0) cl_expect(lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
+            const int32_t e0 = lo + lane;
+            // this level's first-pass row words were loaded one iteration
+            // ago (HBM latency is ~ a few level times); start the next one's
+#pragma unroll
+            for (int q = 0; q < 2 * FEC; q++) w0[q] = wn[q];
+            c0 = cn;
+            if (L + kNWC < a.ell) {
+                const int32_t j = i + 1 - hcb;
+                const int32_t nlo = j < 32 ? __shfl_sync(0xffffffffu, hlo, j) : a.lvl_ptr[L + kNWC];
+                const int32_t nhi = j < 32 ? __shfl_sync(0xffffffffu, hhi, j) : a.lvl_ptr[L + kNWC + 1];
+                load_row(nlo + lane < nhi ? nlo + lane : nlo, wn, cn);
+            }
+            // owner levels <= L-7 in this CTA's ring: the owner warps publish
+            // independently, so wait for every level this warp has not yet
+            // seen (L-14 .. L-7; older ones were covered by its level L-8)
+            const long long t0 = clock64();
+            for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
+                cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
+            const long long t1 = clock64();
+            const unsigned fbar = cl_mapa(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, peer);
+            {
+                const T acc = (a.skip_far & 1) ? T(0) : far_sum(w0, __reduce_max_sync(0xffffffffu, c0));
+                if (e0 < hi) cl_st_async64(cl_mapa(sfar_base + (unsigned)(e0 & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+            }
+            for (int32_t base = lo + 32; base < hi; base += 32) {   // wide levels: further passes
+                const int32_t e = base + lane;
+                uint4 w1[2 * FEC];
+                unsigned c1;
+                load_row(e < hi ? e : base, w1, c1);
+                const T acc = (a.skip_far & 1) ? T(0) : far_sum(w1, __reduce_max_sync(0xffffffffu, c1));
+                if (e < hi) cl_st_async64(cl_mapa(sfar_base + (unsigned)(e & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+            }
+            if (a.dbg && b == 0 && lane == 0) {
+                const long long t2 = clock64();
+                atomicAdd(a.dbg + 4, (unsigned long long)(t1 - t0));
+                atomicAdd(a.dbg + 5, (unsigned long long)(t2 - t1));
+                atomicAdd(a.dbg + 6, 1ull);
+            }
+        }
+        // the owner's last stores into this CTA have landed before it may exit
+        for (int32_t X = max(0, a.ell - kNWC); X < a.ell; X++)
+            cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
+    } else {
+        // --------------------------------------------------- owner warps --
+        int32_t cb = 0;
+        auto ld_bounds = [&](int32_t i0, int32_t &vlo, int32_t &vhi) {
+            const int32_t L = warp + (i0 + lane) * kNWC;
+            vlo = a.lvl_ptr[min(L, a.ell)];
+            vhi = a.lvl_ptr[min(L + 1, a.ell)];
+        };
+        int32_t clo, chi;
+        ld_bounds(0, clo, chi);
+        int32_t staged = 0;
+        for (int32_t i = 0;; i++) {
+            const int32_t L = warp + i * kNWC;
+            if (L >= a.ell) break;
+            if (i - cb == 32) {
+                cb += 32;
+                ld_bounds(cb, clo, chi);
+            }
+            const int32_t lo = __shfl_sync(0xffffffffu, clo, i - cb);
+            const int32_t hi = __shfl_sync(0xffffffffu, chi, i - cb);
+            const int32_t np = min((hi - lo + 31) >> 5, kNP);
+            // arm this level's far-sum phase (the helper's st.async land on it);
+            // phase L-16 completed when this warp consumed level L-16
+            if (lane == 0) cl_expect(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
+            while (staged < hi) staged = df_acq(ctrl);
+            auto level = [&](auto npx) {
+                constexpr int NPX = decltype(npx)::value;
+                auto act = [&](int p) { return NPX == 1 || p < np; };
+                T gx[NPX], sp[NPX];
+                int32_t u[NPX];
+                unsigned rowa[NPX], pn[NPX], cnt[NPX];
+                unsigned nw[NPX][NN / 2];
+#pragma unroll
+                for (int p = 0; p < NPX; p++) {
+                    if (act(p)) {
+                        const int32_t e = lo + 32 * p + lane;
+                        const int32_t ee = e < hi ? e : lo + 32 * p;
+                        const unsigned st = stage_base + ((unsigned)(ee >> lgc) % ns) * sbytes;
+                        const unsigned off = (unsigned)(ee & (ch - 1));
+                        rowa[p] = st + off * (unsigned)a.kpn * 2;
+                        gx[p] = bits_to<T>(df_lds64(st + nbytes + off * 8));
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u[p]) : "r"(st + nbytes + gbytes + off * 4));
+                        const unsigned pc = lds32u(rowa[p] + OFF_PN);
+                        pn[p] = pc & 0xffffu;
+                        cnt[p] = pc >> 16;
+                        df_near_words<NN>(rowa[p] + OFF_NEAR, nw[p]);
+                        u[p] = e < hi ? u[p] : -1;
+                    } else {
+                        gx[p] = T(0);
+                        u[p] = -1;
+                        rowa[p] = pn[p] = cnt[p] = 0;
+#pragma unroll
+                        for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
+                    }
+                }
+                const long long t0 = clock64();
+                wait_lvl(L - kNear - 1);   // mid: levels <= L-3
+                const long long t1 = clock64();
+#pragma unroll
+                for (int p = 0; p < NPX; p++) {
+                    sp[p] = T(0);
+                    if (act(p)) {
+                        const unsigned nm8 = (__reduce_max_sync(0xffffffffu, (cnt[p] >> 5) & 63u) + 7) >> 3;
+                        T acc = T(0);
+                        for (unsigned c = 0; c < nm8; c++) acc += df_sum<T, 8>(ring_base, rowa[p] + 16 * c);
+                        sp[p] = acc;
+                    }
+                }
+                // far sums of this level, from the helper (as late as possible)
+                const long long t2 = clock64();
+                cl_wait(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, (unsigned)((L / kLB) & 1));
+                const long long t2b = clock64();
+                const long long rtt = L >= kMid + 1 ? t2b - pubt[(L - kMid - 1) & 63] : 0;
+#pragma unroll
+                for (int p = 0; p < NPX; p++)
+                    if (act(p))
+                        sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u));
+                unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
+                df_pin(lvl_addr);
+                T gs[NPX], Fx[NPX];
+                unsigned na[NPX][NN], sa[NPX], stp[NPX];
+#pragma unroll
+                for (int p = 0; p < NPX; p++) {
+                    gs[p] = act(p) ? gx[p] - sp[p] : T(0);
+                    df_pin(gs[p]);
+                    sa[p] = ring_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u;
+                    stp[p] = (act(p) && u[p] >= 0) ? 1u : 0u;
+                    df_pin(sa[p]);
+                    df_pin(stp[p]);
+#pragma unroll
+                    for (int q = 0; q < NN / 2; q++) {
+                        na[p][2 * q] = ring_base + (nw[p][q] & 0xffffu);
+                        na[p][2 * q + 1] = ring_base + (nw[p][q] >> 16);
+                        df_pin(na[p][2 * q]);
+                        df_pin(na[p][2 * q + 1]);
+                    }
+                }
+                const long long t3 = clock64();
+                wait_lvl(L - 1);   // near: the critical path
+                if (a.dbg && b == 0 && lane == 0) {
+                    const long long t4 = clock64();
+                    atomicAdd(a.dbg + 0, (unsigned long long)(t2b - t2));
+                    atomicAdd(a.dbg + 1, (unsigned long long)(t4 - t3));
+                    atomicAdd(a.dbg + 2, (unsigned long long)rtt);
+                    atomicAdd(a.dbg + 3, 1ull);
+                }
+                T v[NPX][NN];
+#pragma unroll
+                for (int p = 0; p < NPX; p++)
+#pragma unroll
+                    for (int j = 0; j < NN; j++) v[p][j] = bits_to<T>(df_lds64(na[p][j]));
+#pragma unroll
+                for (int p = 0; p < NPX; p++) {
+#pragma unroll
+                    for (int st = 1; st < NN; st <<= 1)
+#pragma unroll
+                        for (int j = 0; j < NN; j += 2 * st) v[p][j] += v[p][j + st];
+                    Fx[p] = gs[p] - v[p][0];
+                }
+#pragma unroll
+                for (int p = 0; p < NPX; p++) df_stp64(sa[p], df_bits<T>(Fx[p]), stp[p]);
+                if (NPX == kNP) {
+                    // passes beyond kNP: serially, all deps done (far sums in sfar)
+                    for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
+                        const int32_t e = base + lane;
+                        const int32_t ee = e < hi ? e : base;
+                        const unsigned st = stage_base + ((unsigned)(ee >> lgc) % ns) * sbytes;
+                        const unsigned off = (unsigned)(ee & (ch - 1));
+                        const unsigned row = st + off * (unsigned)a.kpn * 2;
+                        const T g1 = bits_to<T>(df_lds64(st + nbytes + off * 8));
+                        int32_t u1;
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + nbytes + gbytes + off * 4));
+                        const unsigned p16 = lds32u(row + OFF_PN) & 0xffffu;
+                        const T s1 = bits_to<T>(df_lds64(sfar_base + (unsigned)(ee & a.ring_mask) * 8u)) +
+                                     df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
+                        const T F1 = g1 - s1;
+                        if (e < hi) {
+                            const unsigned sl = ring_base + (unsigned)(e & a.ring_mask) * 8u;
+                            asm volatile("st.shared.b64 [%0], %1;" ::"r"(sl), "l"(df_bits<T>(F1)) : "memory");
+                            cl_st_async64(cl_mapa(sl, peer), df_bits<T>(F1), cl_mapa(lvl_addr, peer));
+                            f[(size_t)u1 * a.B + b] = F1 - bits_to<T>(df_lds64(ring_base + p16));
+                        }
+                    }
+                }
+                // publish locally (critical path)
+                __syncwarp();
+                asm volatile(
+                    "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
+                    "@q mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
+                    "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
+                    "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
+                    : "memory");
+                if (a.dbg && lane == 0) pubt[L & 63] = clock64();
+                // forward F to the helper's ring: each store completes its bytes
+                // on the helper's lvlbar[L % kLB] (armed there with 8 * width)
+                {
+                    const unsigned rbar = cl_mapa(lvl_addr, peer);
+#pragma unroll
+                    for (int p = 0; p < NPX; p++)
+                        if (stp[p]) cl_st_async64(cl_mapa(sa[p], peer), df_bits<T>(Fx[p]), rbar);
+                }
+#pragma unroll
+                for (int p = 0; p < NPX; p++)
+                    if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
+            };
+            if (np <= 1)
+                level(std::integral_constant<int, 1>{});
+            else
+                level(std::integral_constant<int, kNP>{});
+        }
+    }
+    __syncwarp();
+    cl_sync();   // neither CTA exits while its peer may still write into its shared memory
+}
+
+static size_t ringcl_smem_bytes(const RingDFPlan &R) {   // owner stages; the helper stages nothing
+    const size_t so = (size_t)R.nstage * R.ch * ((size_t)R.kpn * 2 + 12);
+    return (size_t)(2 * R.ring + 16) * 8 + 8 * (size_t)(kMaxStageCL + 2 * kLB) + 48 + so;
+}
+
+void ringcl_plan(RingDFPlan &R) {
+    R.ch_h = R.ch;
+    R.nstage_h = R.nstage;
+    R.cl_ok = R.ok && R.fe <= 128 && ringcl_smem_bytes(R) <= kSmemCapDF;
+}
+
+bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
+
+cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
+                                  int dtype, const void *gP, void *f, int64_t B, cudaStream_t s) {
+    if (P.n == 0) return cudaSuccess;
+    if (!ringcl_fits(R)) return cudaErrorInvalidConfiguration;
+    RDFArgs a{};
+    a.Dn = R.D;
+    a.Df = R.D + R.npad * R.kpn;
+    a.gP = gP;
+    a.ru = ru_pad;
+    a.lvl_ptr = P.lvl_ptr;
+    a.f = f;
+    a.npad = R.npad;
+    a.n = P.n;
+    a.kpn = R.kpn;
+    a.kpf = R.kpf;
+    a.fe = R.fe;
+    a.ell = P.ell;
+    a.B = (int32_t)B;
+    a.ring_mask = R.ring - 1;
+    a.lg_ch = 0;
+    while ((1 << a.lg_ch) < R.ch) a.lg_ch++;
+    a.nstage = R.nstage;
+    a.lg_chh = 0;
+    while ((1 << a.lg_chh) < R.ch_h) a.lg_chh++;
+    a.nstage_h = R.nstage_h;
+    a.dbg = R.prof ? R.dbg : nullptr;   // ring_debug bit 3: wait-time counters
+    a.skip_far = R.skip_far;            // timing experiments only
+    const size_t smem = ringcl_smem_bytes(R);
+    void *fn = nullptr;
+#define RCL_FN(NN, NM, FEC)                                                                    \
+    if (R.nn == NN && R.nm == NM && R.fe <= 16 * FEC)                                          \
+        fn = dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC> : (void *)k_moeb_ringcl<double, NN, NM, FEC>;
+#define RCL_NM(NN, FEC) RCL_FN(NN, 16, FEC) RCL_FN(NN, 32, FEC)
+#define RCL_FE(FEC) RCL_NM(4, FEC) RCL_NM(8, FEC) RCL_NM(16, FEC)
+    RCL_FE(8)
+#undef RCL_FE
+#undef RCL_NM
+#undef RCL_FN
+    if (!fn) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * B));
+    cfg.blockDim = dim3(32 * (kNWC + 1));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *args[] = {&a};
+    launches_add(1);
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace poset

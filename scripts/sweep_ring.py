@@ -30,7 +30,7 @@ for lpe in (1, 2, 4, 8):
     res[f"lpe{lpe}_clk_per_level"] = ms * 1e-3 * 1.965e9 / info["ell"]
 for kern, name in ((pz.MOEB_RINGDF, "ringdf"), (pz.MOEB_RINGWS, "ringws"), (pz.MOEB_RING, "ring_lpe8")):
     if (kern == pz.MOEB_RINGWS and not info["ringws"]) or (kern == pz.MOEB_RINGDF and not info["ringdf"] & 1) \
-            or (kern == pz.MOEB_RINGFR and not info["ringdf"] & 2):
+            or (kern == pz.MOEB_RINGCL and not info["ringdf"] & 2):
         continue
     P.set_option("ring_lpe", 8)
     P.set_option("moebius_kernel", kern)

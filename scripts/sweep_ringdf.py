@@ -30,6 +30,26 @@ def clk(kern):
 
 
 res["ringdf_clk"] = clk(pz.MOEB_RINGDF)
+if info["ringdf"] & 2:
+    res["ringcl_clk"] = clk(pz.MOEB_RINGCL)
+    P.set_option("ring_debug", 8)
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    d = P.debug_read()
+    lv, hl = max(1, int(d[3])), max(1, int(d[6]))
+    res["ringcl_prof"] = {"owner_farbar_wait": d[0] / lv, "owner_near_wait": d[1] / lv, "owner_L7pub_to_far_ready": d[2] / lv,
+                          "helper_lvl_waits": d[4] / hl, "helper_far_sum_send": d[5] / hl, "levels": lv}
+    P.set_option("ring_debug", 16)
+    res["ringcl_nofar_clk"] = clk(pz.MOEB_RINGCL)
+    P.set_option("ring_debug", 24)
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    d = P.debug_read()
+    lv, hl = max(1, int(d[3])), max(1, int(d[6]))
+    res["ringcl_nofar_prof"] = {"owner_farbar_wait": d[0] / lv, "owner_near_wait": d[1] / lv, "owner_L7pub_to_far_ready": d[2] / lv,
+                          "helper_lvl_waits": d[4] / hl, "helper_far_sum_send": d[5] / hl}
+    P.set_option("ring_debug", 0)
+    xi = torch.from_numpy(W.int_values(wl.n, 4, -1000, 1000, seed=5)).cuda()
+    P.set_option("moebius_kernel", pz.MOEB_RINGCL)
+    res["ok_roundtrip_i64_ringcl"] = bool((P.moebius(P.zeta(xi)) == xi).all())
 res["ringdf_fp64_maxerr_vs_input"] = float((y - x).abs().max())
 P.set_option("ring_debug", 8)
 P.moebius(g, out=y); torch.cuda.synchronize()

@@ -22,7 +22,7 @@ from oracle import brute  # noqa: E402
 from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
 
 KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING, pz.MOEB_CSR, pz.MOEB_RINGWS,
-           pz.MOEB_RINGDF]
+           pz.MOEB_RINGDF, pz.MOEB_RINGCL]
 
 
 def kernels_for(P):
@@ -31,7 +31,8 @@ def kernels_for(P):
     info = P.info()
     return [k for k in KERNELS
             if (k != pz.MOEB_RING or info["dist_bytes"] > 0) and (k != pz.MOEB_CSR or info["csr_bytes"] > 0)
-            and (k != pz.MOEB_RINGWS or info["ringws"]) and (k != pz.MOEB_RINGDF or info["ringdf"] & 1)]
+            and (k != pz.MOEB_RINGWS or info["ringws"]) and (k != pz.MOEB_RINGDF or info["ringdf"] & 1)
+            and (k != pz.MOEB_RINGCL or info["ringdf"] & 2)]
 facts = load_facts()
 PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
 
@@ -215,7 +216,7 @@ def test_ring_schedule_selection_and_limits():
     P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
     info = P.info()
     assert info["dist_bytes"] > 0 and 0 < info["reach"] < 65535
-    assert info["moebius_kernel"] == pz.MOEB_RINGDF and info["ringws"] == 1 and info["ringdf"] & 1
+    assert info["moebius_kernel"] == pz.MOEB_RINGCL and info["ringws"] == 1 and info["ringdf"] == 3
     for B in (1, 2, 7, 33):
         f = W.int_values(n, B, -1000, 1000, seed=B)
         g = gpu_zeta(P, f)
@@ -225,9 +226,8 @@ def test_ring_schedule_selection_and_limits():
         assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), B
         assert (gpu_moebius(P, h, pz.MOEB_RINGWS) == want).all(), B
         assert (gpu_moebius(P, h, pz.MOEB_RINGDF) == want).all(), B
-        with pytest.raises(pz.PosetError):   # RINGFR was removed (slower than RINGDF)
-            gpu_moebius(P, h, pz.MOEB_RINGFR)
-        P.set_option("moebius_kernel", pz.MOEB_AUTO)
+        assert info["ringdf"] & 2
+        assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), B
         for lpe in (1, 2, 4, 8):
             P.set_option("ring_lpe", lpe)
             assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), (B, lpe)
