@@ -44,6 +44,7 @@ static constexpr int kLB = 16;     // level-completion mbarriers (ring), > kMid 
 static constexpr int kNP = 3;      // passes of 32 elements kept in registers per level
 static constexpr int kNWC = 8;     // consumer warps (levels round-robin)
 static constexpr int kMaxStageCL = 32;   // RINGCL stage barriers
+static constexpr int kNWH = 16;          // RINGCL block: 16 warps (helper: 2 per level group)
 
 // ------------------------------------------------------------ setup -------
 // max over ranks of (#deps at level distance <= kNear, #deps in (kNear, kMid])
@@ -865,7 +866,7 @@ __device__ __forceinline__ void cl_sync() {
 }
 
 template <typename T, int NN, int NM, int FEC>
-__global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
+__global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN);
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
@@ -876,8 +877,8 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
     const int lgc = owner ? a.lg_ch : a.lg_chh;
     const int ch = 1 << lgc;
     const unsigned ring_base = smem_u32(smem);                         // RING + 16 entries
-    const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // RING entries (owner)
-    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(2 * RING + 16) * 8);
+    const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // 2 x RING entries (owner)
+    u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(3 * RING + 16) * 8);
     constexpr int nb = kMaxStageCL + 2 * kLB;   // stage | lvlbar | farbar
     const unsigned lvl_u32 = smem_u32(bars + kMaxStageCL), far_u32 = lvl_u32 + kLB * 8;
     unsigned *ctrl_p = reinterpret_cast<unsigned *>(bars + nb);   // ready | done | prog[8]
@@ -911,9 +912,9 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
         if (Ld < 0) return;
         cl_wait_cta(lvl_u32 + (unsigned)(Ld & (kLB - 1)) * 8u, (unsigned)((Ld / kLB) & 1));
     };
-    if (warp == kNWC) {
+    if (owner && warp == kNWC) {
         // ------------------------------------------------------ producer --
-        if (owner && lane == 0) {
+        if (lane == 0) {
             auto issue = [&](int32_t c) {
                 const int s = (int)((unsigned)c % ns);
                 unsigned char *st = stage0 + (size_t)s * sbytes;
@@ -959,16 +960,22 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
         // before the wait for the owner's levels (their latency hides behind
         // it); no staging, so no coupling between the out-of-order helper
         // warps and a stage ring.
+        // Two warps per level (kNWH = 16): warp (g, hh) = (warp % 8, warp / 8)
+        // owns the levels L = g (mod 8) and the chunks c = hh (mod 2) of their
+        // far rows, halving the latency of a level's far sum; the owner adds
+        // the two partial sums (sfar[0], sfar[1]).
+        const int g = warp & (kNWC - 1), hh = warp / kNWC;
+        const unsigned sfar_h = sfar_base + (unsigned)(hh * RING) * 8u;
         int32_t hcb = 0, hlo, hhi;   // level bounds of this warp's next 32 levels, in registers
-        hlo = a.lvl_ptr[min(warp + lane * kNWC, a.ell)];
-        hhi = a.lvl_ptr[min(warp + lane * kNWC + 1, a.ell)];
-        auto far_sum = [&](const uint4 (&w)[2 * FEC], unsigned nf) -> T {
+        hlo = a.lvl_ptr[min(g + lane * kNWC, a.ell)];
+        hhi = a.lvl_ptr[min(g + lane * kNWC + 1, a.ell)];
+        auto far_sum = [&](const uint4 (&w)[FEC], unsigned nf) -> T {
             T acc = T(0);
 #pragma unroll
-            for (int c = 0; c < FEC; c++) {
-                if ((unsigned)c >= nf) break;   // warp-uniform: the group's colour count
-                const unsigned ws[8] = {w[2 * c].x, w[2 * c].y, w[2 * c].z, w[2 * c].w,
-                                        w[2 * c + 1].x, w[2 * c + 1].y, w[2 * c + 1].z, w[2 * c + 1].w};
+            for (int j = 0; j < FEC / 2; j++) {
+                if ((unsigned)(2 * j + hh) >= nf) break;   // warp-uniform: the group's colour count
+                const unsigned ws[8] = {w[2 * j].x, w[2 * j].y, w[2 * j].z, w[2 * j].w,
+                                        w[2 * j + 1].x, w[2 * j + 1].y, w[2 * j + 1].z, w[2 * j + 1].w};
                 T v[16];
 #pragma unroll
                 for (int h = 0; h < 8; h++) {
@@ -983,35 +990,39 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
             }
             return acc;
         };
-        auto load_row = [&](int32_t ee, uint4 (&w)[2 * FEC], unsigned &c16) {
+        auto load_row = [&](int32_t ee, uint4 (&w)[FEC], unsigned &c16) {
             const uint4 *rg = reinterpret_cast<const uint4 *>(a.Df + (size_t)ee * a.kpf);
             const int nq = a.fe / 8;   // the row's 16-byte words (fe <= 16 * FEC)
 #pragma unroll
-            for (int q = 0; q < 2 * FEC; q++) w[q] = q < nq ? __ldg(rg + q) : make_uint4(0, 0, 0, 0);
+            for (int j = 0; j < FEC / 2; j++) {   // chunk 2j + hh = words 4j + 2hh, +1
+                const int q = 4 * j + 2 * hh;
+                w[2 * j] = q < nq ? __ldg(rg + q) : make_uint4(0, 0, 0, 0);
+                w[2 * j + 1] = q + 1 < nq ? __ldg(rg + q + 1) : make_uint4(0, 0, 0, 0);
+            }
             c16 = __ldg(a.Df + (size_t)ee * a.kpf + a.fe);   // 16-entry chunks used by this row's group
         };
-        uint4 w0[2 * FEC], wn[2 * FEC];
+        uint4 w0[FEC], wn[FEC];
         unsigned c0 = 0, cn = 0;
-        if (warp < a.ell) {
+        if (g < a.ell) {
             const int32_t lo0 = __shfl_sync(0xffffffffu, hlo, 0), hi0 = __shfl_sync(0xffffffffu, hhi, 0);
             load_row(lo0 + lane < hi0 ? lo0 + lane : lo0, wn, cn);
         }
-        for (int32_t L = warp, i = 0; L < a.ell; L += kNWC, i++) {
+        for (int32_t L = g, i = 0; L < a.ell; L += kNWC, i++) {
             if (i - hcb == 32) {
                 hcb += 32;
-                hlo = a.lvl_ptr[min(warp + (hcb + lane) * kNWC, a.ell)];
-                hhi = a.lvl_ptr[min(warp + (hcb + lane) * kNWC + 1, a.ell)];
+                hlo = a.lvl_ptr[min(g + (hcb + lane) * kNWC, a.ell)];
+                hhi = a.lvl_ptr[min(g + (hcb + lane) * kNWC + 1, a.ell)];
             }
             const int32_t lo = __shfl_sync(0xffffffffu, hlo, i - hcb), hi = __shfl_sync(0xffffffffu, hhi, i - hcb);
             // arm this level's phase: the owner's F values of level L land here
             // with st.async (8 bytes per element); phase L-16 is complete (this
             // warp waited for it at level L-8)
-            if (lane == 0) cl_expect(lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
+            if (hh == 0 && lane == 0) cl_expect(lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
             const int32_t e0 = lo + lane;
             // this level's first-pass row words were loaded one iteration
             // ago (HBM latency is ~ a few level times); start the next one's
 #pragma unroll
-            for (int q = 0; q < 2 * FEC; q++) w0[q] = wn[q];
+            for (int q = 0; q < FEC; q++) w0[q] = wn[q];
             c0 = cn;
             if (L + kNWC < a.ell) {
                 const int32_t j = i + 1 - hcb;
@@ -1026,30 +1037,36 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
             for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
                 cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
             const long long t1 = clock64();
+            long long t1b = t1;
             const unsigned fbar = cl_mapa(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, peer);
             {
                 const T acc = (a.skip_far & 1) ? T(0) : far_sum(w0, __reduce_max_sync(0xffffffffu, c0));
-                if (e0 < hi) cl_st_async64(cl_mapa(sfar_base + (unsigned)(e0 & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+                if (a.dbg) {   // instrumentation: the sum is complete here
+                    asm volatile("" ::"l"(df_bits<T>(acc)));
+                    t1b = clock64();
+                }
+                if (e0 < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e0 & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
             }
             for (int32_t base = lo + 32; base < hi; base += 32) {   // wide levels: further passes
                 const int32_t e = base + lane;
-                uint4 w1[2 * FEC];
+                uint4 w1[FEC];
                 unsigned c1;
                 load_row(e < hi ? e : base, w1, c1);
                 const T acc = (a.skip_far & 1) ? T(0) : far_sum(w1, __reduce_max_sync(0xffffffffu, c1));
-                if (e < hi) cl_st_async64(cl_mapa(sfar_base + (unsigned)(e & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+                if (e < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
             }
-            if (a.dbg && b == 0 && lane == 0) {
+            if (a.dbg && b == 0 && lane == 0 && hh == 0) {
                 const long long t2 = clock64();
                 atomicAdd(a.dbg + 4, (unsigned long long)(t1 - t0));
                 atomicAdd(a.dbg + 5, (unsigned long long)(t2 - t1));
                 atomicAdd(a.dbg + 6, 1ull);
+                atomicAdd(a.dbg + 7, (unsigned long long)(t1b - t1));
             }
         }
         // the owner's last stores into this CTA have landed before it may exit
         for (int32_t X = max(0, a.ell - kNWC); X < a.ell; X++)
             cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
-    } else {
+    } else if (warp < kNWC) {
         // --------------------------------------------------- owner warps --
         int32_t cb = 0;
         auto ld_bounds = [&](int32_t i0, int32_t &vlo, int32_t &vhi) {
@@ -1072,7 +1089,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
             const int32_t np = min((hi - lo + 31) >> 5, kNP);
             // arm this level's far-sum phase (the helper's st.async land on it);
             // phase L-16 completed when this warp consumed level L-16
-            if (lane == 0) cl_expect(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
+            if (lane == 0) cl_expect(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, 16u * (unsigned)(hi - lo));
             while (staged < hi) staged = df_acq(ctrl);
             auto level = [&](auto npx) {
                 constexpr int NPX = decltype(npx)::value;
@@ -1125,7 +1142,8 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
 #pragma unroll
                 for (int p = 0; p < NPX; p++)
                     if (act(p))
-                        sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u));
+                        sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u)) +
+                                 bits_to<T>(df_lds64(sfar_base + (unsigned)(RING + ((lo + 32 * p + lane) & a.ring_mask)) * 8u));
                 unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
                 df_pin(lvl_addr);
                 T gs[NPX], Fx[NPX];
@@ -1183,6 +1201,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
                         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + nbytes + gbytes + off * 4));
                         const unsigned p16 = lds32u(row + OFF_PN) & 0xffffu;
                         const T s1 = bits_to<T>(df_lds64(sfar_base + (unsigned)(ee & a.ring_mask) * 8u)) +
+                                     bits_to<T>(df_lds64(sfar_base + (unsigned)(RING + (ee & a.ring_mask)) * 8u)) +
                                      df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
                         const T F1 = g1 - s1;
                         if (e < hi) {
@@ -1226,7 +1245,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringcl(RDFArgs a) {
 
 static size_t ringcl_smem_bytes(const RingDFPlan &R) {   // owner stages; the helper stages nothing
     const size_t so = (size_t)R.nstage * R.ch * ((size_t)R.kpn * 2 + 12);
-    return (size_t)(2 * R.ring + 16) * 8 + 8 * (size_t)(kMaxStageCL + 2 * kLB) + 48 + so;
+    return (size_t)(3 * R.ring + 16) * 8 + 8 * (size_t)(kMaxStageCL + 2 * kLB) + 48 + so;
 }
 
 void ringcl_plan(RingDFPlan &R) {
@@ -1280,7 +1299,7 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * B));
-    cfg.blockDim = dim3(32 * (kNWC + 1));
+    cfg.blockDim = dim3(32 * kNWH);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
