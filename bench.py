@@ -145,9 +145,11 @@ def alg_bytes(n, k, B, info=None):
     if info is not None and info.get("moebius_kernel") == 5:
         d["moebius_solve"] = info["csr_bytes"] + 32 * n * B + 8 * n   # rows, g, F w+r, f
     if info is not None and info.get("moebius_kernel") in (4, 6, 7, 8):
-        # RING: distance table once (shared by the B CTAs through L2), gP read,
-        # f written, rank->user rows; F never leaves shared memory
-        d["moebius_solve"] = info["dist_bytes"] + 16 * n * B + 4 * n
+        # ring schedules: the schedule's own tables once (shared by the B CTAs
+        # through L2), gP read, f written, rank->user rows; F never leaves
+        # shared memory (RINGCL: nor the far sums -- DSMEM)
+        tab = {4: "ring_bytes", 6: "rws_bytes", 7: "rdf_bytes", 8: "rdf_bytes"}[info["moebius_kernel"]]
+        d["moebius_solve"] = info.get(tab, info["dist_bytes"]) + 16 * n * B + 4 * n
     return d
 
 

@@ -112,6 +112,9 @@ typedef struct {
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
     int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
     int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGCL available       */
+    int64_t rdf_bytes;    /* bytes of the RINGDF / RINGCL near + far tables         */
+    int64_t ring_bytes;   /* bytes of the RING tables (dist + next slot)            */
+    int64_t rws_bytes;    /* bytes of the RINGWS tables                             */
 } poset_info;
 
 /*

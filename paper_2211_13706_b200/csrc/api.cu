@@ -233,6 +233,9 @@ static poset_status finish_setup(poset_s *h) {
                    (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
     I.ringdf = h->rdf.ok ? (ringcl_fits(h->rdf) ? 3 : 1) : 0;   // bit 1: RINGCL
+    I.ring_bytes = h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0;
+    I.rws_bytes = h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0;
+    I.rdf_bytes = h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0;
     I.t_dist = t3 - t2;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;

@@ -806,17 +806,23 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
 // a second SM's shared-memory pipe and issue slots take the far sums.
 //   owner  (cluster rank 0): the level pipeline of RINGDF -- rows (near
 //          table), mid sums, the near wait, F into its ring -- but the far
-//          sum of each element comes from the helper through DSMEM (sfar,
-//          announced on farbar[L % kLB]).  After publishing level L locally it
-//          forwards F to the helper's ring (st.shared::cluster) and arrives
-//          (release.cluster) on the helper's lvlbar[L % kLB].
-//   helper (cluster rank 1): 8 warps own levels round-robin; once the
-//          owner's levels <= L-7 have arrived (its lvlbar phases L-14 ..
-//          L-7; older ones it saw at level L-8) it sums the far entries of
-//          level L (far table, bank-coloured) and writes the sums into the
-//          owner's sfar, then arrives on the owner's farbar[L % kLB].
+//          sum of each element comes from the helper through DSMEM (two
+//          partial sums in sfar[0..1], landing on farbar[L % kLB], armed by
+//          the owner with 16 bytes per element).  After publishing level L
+//          locally it forwards F to the helper's ring with st.async, each
+//          store completing 8 bytes on the helper's lvlbar[L % kLB].
+//   helper (cluster rank 1): 16 warps; warps g and g+8 own the levels
+//          L = g (mod 8) and the even / odd 16-entry chunks of their far rows.
+//          A warp arms lvlbar[L % kLB] (8 bytes per element), prefetches the
+//          next level's far rows from global memory into registers, waits
+//          for the owner's levels L-14 .. L-7 (they are published out of
+//          order; older ones it saw at level L-8), sums and st.async's its
+//          partial sums to the owner.
 // Slack: the far sum of level L is needed when level L-1 completes, i.e.
-// 6 level times after level L-7 completed -- enough for two DSMEM hops.
+// 6 level times after level L-7 completed (a DSMEM round trip is ~320
+// cycles).  Waits are CTA-scope try_waits: the bytes are made visible by the
+// complete_tx mechanism, and a cluster-scope acquire would cost an L1
+// invalidate (CCTL.IVALL) per wait.
 __device__ __forceinline__ unsigned cl_rank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
