@@ -1039,6 +1039,10 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             // owner levels <= L-7 in this CTA's ring: the owner warps publish
             // independently, so wait for every level this warp has not yet
             // seen (L-14 .. L-7; older ones were covered by its level L-8)
+            if (a.dbg && (a.skip_far & 2)) {   // instrumentation: wait for this level's row words here
+#pragma unroll
+                for (int q = 0; q < FEC; q++) asm volatile("" ::"r"(w0[q].x), "r"(w0[q].y), "r"(w0[q].z), "r"(w0[q].w));
+            }
             const long long t0 = clock64();
             for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
                 cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
@@ -1292,11 +1296,12 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     const size_t smem = ringcl_smem_bytes(R);
     void *fn = nullptr;
 #define RCL_FN(NN, NM, FEC)                                                                    \
-    if (R.nn == NN && R.nm == NM && R.fe <= 16 * FEC)                                          \
+    if (R.nn == NN && R.nm == NM && fec == FEC)                                                \
         fn = dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC> : (void *)k_moeb_ringcl<double, NN, NM, FEC>;
 #define RCL_NM(NN, FEC) RCL_FN(NN, 16, FEC) RCL_FN(NN, 32, FEC)
 #define RCL_FE(FEC) RCL_NM(4, FEC) RCL_NM(8, FEC) RCL_NM(16, FEC)
-    RCL_FE(8)
+    const int fec = R.fe <= 64 ? 4 : R.fe <= 96 ? 6 : 8;   // chunks per row, split by parity
+    RCL_FE(4) RCL_FE(6) RCL_FE(8)
 #undef RCL_FE
 #undef RCL_NM
 #undef RCL_FN

@@ -38,6 +38,12 @@ if info["ringdf"] & 2:
     lv, hl = max(1, int(d[3])), max(1, int(d[6]))
     res["ringcl_prof"] = {"owner_farbar_wait": d[0] / lv, "owner_near_wait": d[1] / lv, "owner_L7pub_to_far_ready": d[2] / lv,
                           "helper_lvl_waits": d[4] / hl, "helper_far_sum_send": d[5] / hl, "helper_far_sum_only": d[7] / hl, "levels": lv}
+    P.set_option("ring_debug", 8 + 32)   # bit 5 (skip_far & 2): rows awaited before the waits
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    d = P.debug_read()
+    lv, hl = max(1, int(d[3])), max(1, int(d[6]))
+    res["ringcl_prof_rowsfirst"] = {"helper_lvl_waits": d[4] / hl, "helper_far_sum_send": d[5] / hl,
+                                    "helper_far_sum_only": d[7] / hl}
     P.set_option("ring_debug", 16)
     res["ringcl_nofar_clk"] = clk(pz.MOEB_RINGCL)
     P.set_option("ring_debug", 24)
