@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(RING + tid) * 8), "l"(0ull) : "memory");
     if (tid == 0) {
         for (int s = 0; s < a.nstage; s++) mbar_init(&bars[s], 1);
-        for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 1);
+        for (int s = 0; s < kLB; s++) mbar_init(&bars[a.nstage + s], 32);   // one arrival per lane
         asm volatile("st.shared.s32 [%0], 0;\n\tst.shared.s32 [%0+4], 0;\n\tst.shared.s32 [%0+8], 0;" ::"r"(ctrl)
                      : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -651,12 +651,13 @@ __global__ void __launch_bounds__(32 * (kNWC + 1)) k_moeb_ringdf(RDFArgs a) {
             }
             long long t_pre = 0;
             if (PROF) t_pre = clock64();
-            // publish: __syncwarp orders the lanes' ring stores before lane 0's
-            // single release-arrive; lane 0 also advances done_rank (producer)
-            __syncwarp();
+            // publish: every lane arrives (release: its own ring store is
+            // ordered before its arrival; the phase needs all 32), so neither
+            // a __syncwarp nor a branch sits on the critical path; lane 0 also
+            // advances done_rank (producer)
             asm volatile(
                 "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
-                "@q mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
+                "mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
                 "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
                 "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
                 : "memory");
@@ -909,6 +910,8 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(RING + tid) * 8), "l"(0ull) : "memory");
     if (tid == 0) {
         for (int s = 0; s < nb; s++) mbar_init(&bars[s], 1);
+        if (owner)   // the owner's level barriers take one arrival per lane
+            for (int s = 0; s < kLB; s++) mbar_init(&bars[kMaxStageCL + s], 32);
         for (int i = 0; i < 10; i++) ctrl_p[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1222,11 +1225,10 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         }
                     }
                 }
-                // publish locally (critical path)
-                __syncwarp();
+                // publish locally (critical path): all 32 lanes arrive
                 asm volatile(
                     "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
-                    "@q mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
+                    "mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
                     "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
                     "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
                     : "memory");
