@@ -872,7 +872,7 @@ __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <typename T, int NN, int NM, int FEC>
+template <typename T, int NN, int NM, int FEC, bool PROF = false>
 __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN);
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1042,19 +1042,19 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             // owner levels <= L-7 in this CTA's ring: the owner warps publish
             // independently, so wait for every level this warp has not yet
             // seen (L-14 .. L-7; older ones were covered by its level L-8)
-            if (a.dbg && (a.skip_far & 2)) {   // instrumentation: wait for this level's row words here
+            if (PROF && (a.skip_far & 2)) {   // instrumentation: wait for this level's row words here
 #pragma unroll
                 for (int q = 0; q < FEC; q++) asm volatile("" ::"r"(w0[q].x), "r"(w0[q].y), "r"(w0[q].z), "r"(w0[q].w));
             }
-            const long long t0 = clock64();
+            const long long t0 = PROF ? clock64() : 0;
             for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
                 cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
-            const long long t1 = clock64();
+            const long long t1 = PROF ? clock64() : 0;
             long long t1b = t1;
             const unsigned fbar = cl_mapa(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, peer);
             {
                 const T acc = (a.skip_far & 1) ? T(0) : far_sum(w0, __reduce_max_sync(0xffffffffu, c0));
-                if (a.dbg) {   // instrumentation: the sum is complete here
+                if (PROF) {   // instrumentation: the sum is complete here
                     asm volatile("" ::"l"(df_bits<T>(acc)));
                     t1b = clock64();
                 }
@@ -1068,8 +1068,8 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                 const T acc = (a.skip_far & 1) ? T(0) : far_sum(w1, __reduce_max_sync(0xffffffffu, c1));
                 if (e < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
             }
-            if (a.dbg && b == 0 && lane == 0 && hh == 0) {
-                const long long t2 = clock64();
+            if (PROF && b == 0 && lane == 0 && hh == 0) {
+                const long long t2 = PROF ? clock64() : 0;
                 atomicAdd(a.dbg + 4, (unsigned long long)(t1 - t0));
                 atomicAdd(a.dbg + 5, (unsigned long long)(t2 - t1));
                 atomicAdd(a.dbg + 6, 1ull);
@@ -1134,9 +1134,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
                     }
                 }
-                const long long t0 = clock64();
                 wait_lvl(L - kNear - 1);   // mid: levels <= L-3
-                const long long t1 = clock64();
 #pragma unroll
                 for (int p = 0; p < NPX; p++) {
                     sp[p] = T(0);
@@ -1148,10 +1146,10 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                     }
                 }
                 // far sums of this level, from the helper (as late as possible)
-                const long long t2 = clock64();
+                const long long t2 = PROF ? clock64() : 0;
                 cl_wait(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, (unsigned)((L / kLB) & 1));
-                const long long t2b = clock64();
-                const long long rtt = L >= kMid + 1 ? t2b - pubt[(L - kMid - 1) & 63] : 0;
+                const long long t2b = PROF ? clock64() : 0;
+                const long long rtt = PROF && L >= kMid + 1 ? t2b - pubt[(L - kMid - 1) & 63] : 0;
 #pragma unroll
                 for (int p = 0; p < NPX; p++)
                     if (act(p))
@@ -1177,9 +1175,9 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         df_pin(na[p][2 * q + 1]);
                     }
                 }
-                const long long t3 = clock64();
+                const long long t3 = PROF ? clock64() : 0;
                 wait_lvl(L - 1);   // near: the critical path
-                if (a.dbg && b == 0 && lane == 0) {
+                if (PROF && b == 0 && lane == 0) {
                     const long long t4 = clock64();
                     atomicAdd(a.dbg + 0, (unsigned long long)(t2b - t2));
                     atomicAdd(a.dbg + 1, (unsigned long long)(t4 - t3));
@@ -1232,7 +1230,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                     "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
                     "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
                     : "memory");
-                if (a.dbg && lane == 0) pubt[L & 63] = clock64();
+                if (PROF && lane == 0) pubt[L & 63] = clock64();
                 // forward F to the helper's ring: each store completes its bytes
                 // on the helper's lvlbar[L % kLB] (armed there with 8 * width)
                 {
@@ -1299,7 +1297,10 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     void *fn = nullptr;
 #define RCL_FN(NN, NM, FEC)                                                                    \
     if (R.nn == NN && R.nm == NM && fec == FEC)                                                \
-        fn = dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC> : (void *)k_moeb_ringcl<double, NN, NM, FEC>;
+        fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, true>              \
+                                  : (void *)k_moeb_ringcl<double, NN, NM, FEC, true>)          \
+                    : (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC>                    \
+                                  : (void *)k_moeb_ringcl<double, NN, NM, FEC>);
 #define RCL_NM(NN, FEC) RCL_FN(NN, 16, FEC) RCL_FN(NN, 32, FEC)
 #define RCL_FE(FEC) RCL_NM(4, FEC) RCL_NM(8, FEC) RCL_NM(16, FEC)
     const int fec = R.fe <= 64 ? 4 : R.fe <= 96 ? 6 : 8;   // chunks per row, split by parity
