@@ -1047,8 +1047,40 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                 for (int q = 0; q < FEC; q++) asm volatile("" ::"r"(w0[q].x), "r"(w0[q].y), "r"(w0[q].z), "r"(w0[q].w));
             }
             const long long t0 = PROF ? clock64() : 0;
-            for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
-                cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
+            if (L >= kMid + kNWC) {
+                // the seven older phases are almost always complete: test them
+                // together (non-blocking), fall back to waiting one by one
+                unsigned ok;
+                const int32_t X0 = L - kMid - kNWC;
+                asm volatile(
+                    "{\n.reg .pred p0, p1, p2, p3, p4, p5, p6;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p0, [%1], %8;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p1, [%2], %9;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p2, [%3], %10;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p3, [%4], %11;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p4, [%5], %12;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p5, [%6], %13;\n"
+                    "mbarrier.test_wait.parity.shared::cta.b64 p6, [%7], %14;\n"
+                    "and.pred p0, p0, p1;\nand.pred p2, p2, p3;\nand.pred p4, p4, p5;\n"
+                    "and.pred p0, p0, p2;\nand.pred p4, p4, p6;\nand.pred p0, p0, p4;\n"
+                    "selp.u32 %0, 1, 0, p0;\n}\n"
+                    : "=r"(ok)
+                    : "r"(lvl_u32 + (unsigned)((X0 + 0) & (kLB - 1)) * 8u), "r"(lvl_u32 + (unsigned)((X0 + 1) & (kLB - 1)) * 8u),
+                      "r"(lvl_u32 + (unsigned)((X0 + 2) & (kLB - 1)) * 8u), "r"(lvl_u32 + (unsigned)((X0 + 3) & (kLB - 1)) * 8u),
+                      "r"(lvl_u32 + (unsigned)((X0 + 4) & (kLB - 1)) * 8u), "r"(lvl_u32 + (unsigned)((X0 + 5) & (kLB - 1)) * 8u),
+                      "r"(lvl_u32 + (unsigned)((X0 + 6) & (kLB - 1)) * 8u), "r"((unsigned)(((X0 + 0) / kLB) & 1)),
+                      "r"((unsigned)(((X0 + 1) / kLB) & 1)), "r"((unsigned)(((X0 + 2) / kLB) & 1)),
+                      "r"((unsigned)(((X0 + 3) / kLB) & 1)), "r"((unsigned)(((X0 + 4) / kLB) & 1)),
+                      "r"((unsigned)(((X0 + 5) / kLB) & 1)), "r"((unsigned)(((X0 + 6) / kLB) & 1))
+                    : "memory");
+                if (!ok)
+                    for (int32_t X = X0; X < L - kMid - 1; X++)
+                        cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
+                cl_wait(lvl_u32 + (unsigned)((L - kMid - 1) & (kLB - 1)) * 8u, (unsigned)(((L - kMid - 1) / kLB) & 1));
+            } else {
+                for (int32_t X = max(0, L - kMid - kNWC); X <= L - kMid - 1; X++)
+                    cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
+            }
             const long long t1 = PROF ? clock64() : 0;
             long long t1b = t1;
             const unsigned fbar = cl_mapa(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, peer);
