@@ -1,0 +1,137 @@
+// RINGCL helper far sum in isolation (tuning aid): cycles per 16-lane-group
+// far sum of NCH chunks of 16 ring loads (8-byte, conflict-free pattern) + add
+// tree, one warp alone vs ACT warps of the CTA at once.
+#include <cstdio>
+#include <cuda_runtime.h>
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 lds64(unsigned a) { u64 v; asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory"); return v; }
+template <int NCH, int CL>
+__global__ void k(long long *out, int iters, int act, const uint4 *gsrc = nullptr, long long gn = 0) {
+    __shared__ __align__(16) double ring[4112];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 4112; i += blockDim.x) ring[i] = i * 0.5;
+    __syncthreads();
+    const unsigned rb = (unsigned)__cvta_generic_to_shared(ring);
+    // conflict-free words: lane l, position p reads slot ((l & 15) + 16 * (p + 7 * l)) & 4095
+    uint4 w[2 * NCH];
+    __shared__ __align__(8) u64 sbar[2];
+    __shared__ __align__(16) double sink[1024];
+    if (CL == 2) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[0])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[1])));
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+        if (blockIdx.x == 1) {   // peer: st.async stream into CTA 0's sink, completing tx on its sbar[1] (never armed)
+            if (warp == 0) {
+                unsigned ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"((unsigned)__cvta_generic_to_shared(&sink[lane])));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"((unsigned)__cvta_generic_to_shared(&sbar[1])));
+                for (int i = 0; i < 200000; i++) {
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"((u64)i), "r"(rb) : "memory");
+                    __nanosleep(200);
+                }
+            }
+            asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+            return;
+        }
+    } else if (CL && blockIdx.x) return;   // cluster launch: only CTA 0 measures
+    for (int c = 0; c < 2 * NCH; c++) {
+        unsigned x[4];
+        for (int h = 0; h < 4; h++) {
+            const int p0 = 8 * c + 2 * h, p1 = p0 + 1;
+            const unsigned s0 = (((lane & 15) + 16 * (p0 + 7 * lane)) & 4095) * 8, s1 = (((lane & 15) + 16 * (p1 + 7 * lane)) & 4095) * 8;
+            x[h] = s0 | (s1 << 16);
+        }
+        w[c] = make_uint4(x[0], x[1], x[2], x[3]);
+    }
+    double acc = 0;
+    if (gsrc && warp >= 8) {   // background: streaming 16-byte global loads (HBM misses)
+        unsigned x = 0;
+        for (long long i = (long long)(warp - 8) * 32 + lane; i < gn; i += 8 * 32) {
+            const uint4 v = __ldg(gsrc + i * 7 % gn);
+            x ^= v.x;
+        }
+        if (x == 0x12345) out[1] = x;
+        return;
+    }
+    long long t0 = clock64();
+    if (warp < act) {
+        for (int it = 0; it < iters; it++) {
+            double s = 0;
+#pragma unroll
+            for (int c = 0; c < NCH; c++) {
+                const unsigned ws[8] = {w[2 * c].x, w[2 * c].y, w[2 * c].z, w[2 * c].w, w[2 * c + 1].x, w[2 * c + 1].y, w[2 * c + 1].z, w[2 * c + 1].w};
+                double v[16];
+#pragma unroll
+                for (int h = 0; h < 8; h++) {
+                    v[2 * h] = __longlong_as_double(lds64(rb + (ws[h] & 0xffffu)));
+                    v[2 * h + 1] = __longlong_as_double(lds64(rb + (ws[h] >> 16)));
+                }
+#pragma unroll
+                for (int st = 1; st < 16; st <<= 1)
+#pragma unroll
+                    for (int j = 0; j < 16; j += 2 * st) v[j] += v[j + st];
+                s += v[0];
+            }
+            acc += s;
+            // serialise iterations like a dependent level
+            asm volatile("" ::"d"(acc));
+            w[0].x ^= (unsigned)(acc == 12345.0);
+        }
+    }
+    long long t1 = clock64();
+    if (lane == 0 && warp == 0) out[0] = (t1 - t0) / iters;
+    if (CL == 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+    if (acc == 1.0) out[1] = 1;
+}
+template <int CL>
+void run_cl(long long *d, int act) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL ? 2 : 1);
+    cfg.blockDim = dim3(512);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = CL ? 1 : 0;
+    int iters = 2000;
+    const uint4 *gz = nullptr;
+    long long gnz = 0;
+    cudaLaunchKernelEx(&cfg, k<3, CL>, d, iters, act, gz, gnz);
+}
+int main() {
+    long long *d, h;
+    cudaMalloc(&d, 16);
+    for (int act : {1, 16}) {
+        run_cl<2>(d, act);
+        cudaDeviceSynchronize();
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("CLUSTER + peer st.async stream, %2d active warps: %lld cycles (%s)\n", act, h, cudaGetErrorString(cudaGetLastError()));
+        run_cl<1>(d, act);
+        cudaDeviceSynchronize();
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("CLUSTER launch, 3 chunks, %2d active warps: %lld cycles (%s)\n", act, h, cudaGetErrorString(cudaGetLastError()));
+    }
+    for (int act : {1, 2, 4, 16}) {
+        k<3, 0><<<1, 512>>>(d, 2000, act);
+        cudaDeviceSynchronize();
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("3 chunks, %2d active warps: %lld cycles per far sum (warp 0)\n", act, h);
+    }
+    uint4 *g;
+    const long long gn = 1ll << 26;   // 1 GB
+    cudaMalloc(&g, gn * 16);
+    cudaMemset(g, 1, gn * 16);
+    k<3, 0><<<1, 512>>>(d, 2000, 1, g, gn);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3 chunks, 1 warp + 8 warps streaming LDG: %lld\n", h);
+    k<2, 0><<<1, 512>>>(d, 2000, 1);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("2 chunks, 1 warp: %lld\n", h);
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

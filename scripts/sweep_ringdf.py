@@ -44,6 +44,11 @@ if info["ringdf"] & 2:
     lv, hl = max(1, int(d[3])), max(1, int(d[6]))
     res["ringcl_prof_rowsfirst"] = {"helper_lvl_waits": d[4] / hl, "helper_far_sum_send": d[5] / hl,
                                     "helper_far_sum_only": d[7] / hl}
+    P.set_option("ring_debug", 8 + 64)   # bit 6 (skip_far & 4): time a second far sum
+    P.moebius(g, out=y); torch.cuda.synchronize()
+    d = P.debug_read()
+    hl = max(1, int(d[6]))
+    res["ringcl_prof_second_sum"] = {"helper_far_sum_only": d[7] / hl}
     P.set_option("ring_debug", 16)
     res["ringcl_nofar_clk"] = clk(pz.MOEB_RINGCL)
     P.set_option("ring_debug", 24)
