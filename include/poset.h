@@ -206,10 +206,16 @@ poset_status poset_query(poset_t h, poset_info *out);
 
 /* poset_set_option -- "moebius_kernel" (poset_moebius_kernel value);
  * "ring_lpe" (lanes per element of the RING schedule, tuning);
+ * "ringws_nwo" / "ringws_lpeo" (RINGWS warps / lanes per element, tuning);
  * "gather_variant" (process-wide dense zeta gather for batch % 32 == 0:
- * 0 = per-lane row reuse (default), 1 = lanes over columns, 2 = lanes over ranks);
+ * 0 = per-lane row reuse, 2 chains per step (default), 1 = lanes over
+ * columns, 2 = lanes over ranks, 3 = per-lane row reuse, 4 chains per step);
  * "profile" (0/1): record a CUDA event pair on the call's stream around every
- * kernel phase of subsequent calls (see poset_profile_read). */
+ * kernel phase of subsequent calls (see poset_profile_read);
+ * "ring_debug" (timing experiments only): bit 0 RING without the f store,
+ * bit 3 the instrumented RINGDF / RINGCL instantiation (counters through
+ * poset_debug_read), bits 4-6 RINGDF / RINGCL with the far / mid / near sums
+ * skipped -- bits 0 and 4-6 make the results INVALID. */
 poset_status poset_set_option(poset_t h, const char *key, int64_t value);
 
 /* Profiling phases. */
