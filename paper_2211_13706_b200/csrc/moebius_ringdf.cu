@@ -973,7 +973,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         // owns the levels L = g (mod 8) and the chunks c = hh (mod 2) of their
         // far rows, halving the latency of a level's far sum; the owner adds
         // the two partial sums (sfar[0], sfar[1]).
-        const int g = warp & (kNWC - 1), hh = warp / kNWC;
+        const int g = warp >> 1, hh = warp & 1;   // the two warps of a pair on different SMSPs
         const unsigned sfar_h = sfar_base + (unsigned)(hh * RING) * 8u;
         int32_t hcb = 0, hlo, hhi;   // level bounds of this warp's next 32 levels, in registers
         hlo = a.lvl_ptr[min(g + lane * kNWC, a.ell)];
