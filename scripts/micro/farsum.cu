@@ -36,7 +36,8 @@ __global__ void k(long long *out, int iters, int act, const uint4 *gsrc = nullpt
             asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
             return;
         }
-    } else if (CL && blockIdx.x) return;   // cluster launch: only CTA 0 measures
+    } else if (CL == 1 && blockIdx.x) return;   // cluster launch: only CTA 0 measures
+    else if (CL == 3 && blockIdx.x == 0) return;   // cluster launch: only CTA 1 (rank 1) measures
     for (int c = 0; c < 2 * NCH; c++) {
         unsigned x[4];
         for (int h = 0; h < 4; h++) {
@@ -83,6 +84,7 @@ __global__ void k(long long *out, int iters, int act, const uint4 *gsrc = nullpt
     }
     long long t1 = clock64();
     if (lane == 0 && warp == 0) out[0] = (t1 - t0) / iters;
+    if (CL == 3 && lane == 0 && warp == 0) { unsigned r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); out[1] = r; }
     if (CL == 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
     if (acc == 1.0) out[1] = 1;
 }
@@ -109,6 +111,10 @@ int main() {
         cudaDeviceSynchronize();
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
         printf("CLUSTER + peer st.async stream, %2d active warps: %lld cycles (%s)\n", act, h, cudaGetErrorString(cudaGetLastError()));
+        run_cl<3>(d, act);
+        cudaDeviceSynchronize();
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("CLUSTER rank 1 measures, %2d active warps: %lld cycles (%s)\n", act, h, cudaGetErrorString(cudaGetLastError()));
         run_cl<1>(d, act);
         cudaDeviceSynchronize();
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
