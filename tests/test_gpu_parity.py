@@ -246,6 +246,36 @@ def test_ring_schedule_selection_and_limits():
 
 # ---------------------------------------------------------------- edge cases
 
+def test_ring_schedules_wide_levels_and_large_batch():
+    """A level of three 32-element passes (the multi-pass level body of
+    RINGDF / RINGCL), and a batch too large for CTA pairs (AUTO falls back
+    to RINGDF), bit-exact against O2."""
+    # a width-8 window DAG, then one level of 70 elements (3 passes of 32),
+    # each above two elements of the base's top level
+    n0, wide = 3000, 70
+    s0, d0 = W.window_dag(n0, 2, 8, 3, forced=True)
+    _, _, _, lvl = pz.analyze(n0, s0, d0, want_chains=True)
+    top = np.flatnonzero(lvl == lvl.max())
+    rng = np.random.default_rng(4)
+    new = np.repeat(np.arange(n0, n0 + wide, dtype=np.int64), 2)
+    tgt = top[rng.integers(0, top.shape[0], size=new.shape[0])]
+    n = n0 + wide
+    src, dst = np.concatenate([s0, new]), np.concatenate([d0, tgt])
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    info = P.info()
+    assert info["max_level_width"] > 64   # three passes of 32 in one level
+    if not info["ringdf"] & 1:
+        pytest.skip("RINGDF does not fit this poset")
+    for B in (1, 33):
+        h = W.int_values(n, B, -10**17, 10**17, seed=B + 3)
+        want = O.moebius(h)
+        assert (gpu_moebius(P, h, pz.MOEB_RINGDF) == want).all(), B
+        if info["ringdf"] & 2:
+            assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), B
+    h = W.int_values(n, 80, -10**17, 10**17, seed=11)   # 2 x 80 CTAs > 148 SMs
+    assert (gpu_moebius(P, h) == O.moebius(h)).all()
+
+
 def test_edge_cases_tiny():
     for n, (src, dst) in [(1, W.antichain_dag(1)), (7, W.antichain_dag(7)), (40, W.chain_dag(40)),
                           (2, (np.array([1, 1]), np.array([0, 0])))]:
