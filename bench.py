@@ -310,6 +310,14 @@ def main():
     if dom == "moebius_solve":
         roof["note"] = (f"latency-bound triangular solve: {info['ell']} dependent levels, "
                         f"{1e6 * kernels[dom]['ms_per_call'] / 1e3 / max(info['ell'], 1):.1f} µs per level")
+        # the bound that matters for a dependent level sweep: per-level time
+        # against the measured floor of one level hand-off between two warps
+        # (mbarrier arrive -> try_wait wake, scripts/micro/handoff.cu: 91 cycles)
+        mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
+        cyc = kernels[dom]["ms_per_call"] * 1e-3 * mhz * 1e6 / max(info["ell"], 1)
+        roof["latency"] = {"cycles_per_level": cyc, "floor_cycles_per_level": 91.0,
+                           "floor": "two-warp mbarrier hand-off, measured (scripts/micro/handoff.cu)",
+                           "frac": 91.0 / cyc}
 
     # e2e: C-ABI with pinned host buffers, copies inside the timed region
     e2e = None
