@@ -1010,12 +1010,8 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             }
             c16 = __ldg(a.Df + (size_t)ee * a.kpf + a.fe);   // 16-entry chunks used by this row's group
         };
-        uint4 w0[FEC], wn[FEC];
-        unsigned c0 = 0, cn = 0;
-        if (g < a.ell) {
-            const int32_t lo0 = __shfl_sync(0xffffffffu, hlo, 0), hi0 = __shfl_sync(0xffffffffu, hhi, 0);
-            load_row(lo0 + lane < hi0 ? lo0 + lane : lo0, wn, cn);
-        }
+        uint4 w0[FEC];
+        unsigned c0 = 0;
         for (int32_t L = g, i = 0; L < a.ell; L += kNWC, i++) {
             if (i - hcb == 32) {
                 hcb += 32;
@@ -1028,17 +1024,10 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             // warp waited for it at level L-8)
             if (hh == 0 && lane == 0) cl_expect(lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u, 8u * (unsigned)(hi - lo));
             const int32_t e0 = lo + lane;
-            // this level's first-pass row words were loaded one iteration
-            // ago (HBM latency is ~ a few level times); start the next one's
-#pragma unroll
-            for (int q = 0; q < FEC; q++) w0[q] = wn[q];
-            c0 = cn;
-            if (L + kNWC < a.ell) {
-                const int32_t j = i + 1 - hcb;
-                const int32_t nlo = j < 32 ? __shfl_sync(0xffffffffu, hlo, j) : a.lvl_ptr[L + kNWC];
-                const int32_t nhi = j < 32 ? __shfl_sync(0xffffffffu, hhi, j) : a.lvl_ptr[L + kNWC + 1];
-                load_row(nlo + lane < nhi ? nlo + lane : nlo, wn, cn);
-            }
+            // this level's first-pass row words: their latency hides behind
+            // the wait for the owner's levels below (no second register set
+            // for a prefetch -- registers go to loads in flight)
+            load_row(e0 < hi ? e0 : lo, w0, c0);
             // owner levels <= L-7 in this CTA's ring: the owner warps publish
             // independently, so wait for every level this warp has not yet
             // seen (L-14 .. L-7; older ones were covered by its level L-8)
