@@ -1,0 +1,4 @@
+set -x; mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/r100_gpu_tests.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r100_smoke.log 2>&1
+echo done
