@@ -814,11 +814,11 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
 //          store completing 8 bytes on the helper's lvlbar[L % kLB].
 //   helper (cluster rank 1): 16 warps; warps g and g+8 own the levels
 //          L = g (mod 8) and the even / odd 16-entry chunks of their far rows.
-//          A warp arms lvlbar[L % kLB] (8 bytes per element), prefetches the
-//          next level's far rows from global memory into registers, waits
-//          for the owner's levels L-14 .. L-7 (they are published out of
-//          order; older ones it saw at level L-8), sums and st.async's its
-//          partial sums to the owner.
+//          A warp arms lvlbar[L % kLB] (8 bytes per element), loads its
+//          level's far-row words from global memory into registers (their
+//          latency hides behind the wait), waits for the owner's levels
+//          L-14 .. L-7 (they are published out of order; older ones it saw at
+//          level L-8), sums and st.async's its partial sums to the owner.
 // Slack: the far sum of level L is needed when level L-1 completes, i.e.
 // 6 level times after level L-7 completed (a DSMEM round trip is ~320
 // cycles).  Waits are CTA-scope try_waits: the bytes are made visible by the
