@@ -969,8 +969,9 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         // before the wait for the owner's levels (their latency hides behind
         // it); no staging, so no coupling between the out-of-order helper
         // warps and a stage ring.
-        // Two warps per level (kNWH = 16): warp (g, hh) = (warp % 8, warp / 8)
-        // owns the levels L = g (mod 8) and the chunks c = hh (mod 2) of their
+        // Two warps per level (kNWH = 16): warp (g, hh) = (warp / 2, warp % 2)
+        // (the pair on different SM sub-partitions) owns the levels
+        // L = g (mod 8) and the chunks c = hh (mod 2) of their
         // far rows, halving the latency of a level's far sum; the owner adds
         // the two partial sums (sfar[0], sfar[1]).
         const int g = warp >> 1, hh = warp & 1;   // the two warps of a pair on different SMSPs
