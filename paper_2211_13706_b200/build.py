@@ -28,13 +28,31 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each source to an object in parallel (the template-heavy
+    schedules dominate), then link the shared library."""
     if not force and not _stale():
         return SO
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-o", SO] + [os.path.join(CSRC, f) for f in SOURCES]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2"]
+    jobs = []
+    for f in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(f)[0] + ".o")
+        jobs.append((obj, [NVCC, *flags, "-c", "-o", obj, os.path.join(CSRC, f)]))
+
+    def run(job):
+        if verbose:
+            print(" ".join(job[1]), file=sys.stderr)
+        subprocess.check_call(job[1])
+        return job[0]
+
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(run, jobs))
+    link = [NVCC, *ARCH, "-shared", "-o", SO] + objs
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.check_call(link)
     return SO
 
 
