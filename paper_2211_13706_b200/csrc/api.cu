@@ -433,7 +433,7 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         }
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
         if (which == MOEB_RINGCL)
-            CK(launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
+            CK(launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s));
         else
             CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
         return POSET_OK;

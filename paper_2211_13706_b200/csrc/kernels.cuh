@@ -135,6 +135,7 @@ struct RingDFPlan {
     int32_t wmax = 0;                 // widest level
     int32_t ch_h = 0, nstage_h = 0;   // RINGCL helper staging
     bool cl_ok = false;               // RINGCL fits shared memory
+    int32_t nh_max = 1;               // RINGCL helper CTAs per column (1 or 2)
     int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only
@@ -154,7 +155,7 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
 bool ringcl_fits(const RingDFPlan &R);
 void ringcl_plan(RingDFPlan &R);
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
+                                  int dtype, const void *gP, void *f, int64_t batch, int num_sms, cudaStream_t s);
 
 // ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----
 struct CsrRows {

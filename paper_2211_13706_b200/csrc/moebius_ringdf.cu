@@ -872,19 +872,23 @@ __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <typename T, int NN, int NM, int FEC, bool PROF = false>
+template <typename T, int NN, int NM, int FEC, bool PROF = false, int NH = 1>
 __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
+    // NH helper CTAs (cluster of NH + 1); the far chunks of a row are split
+    // over the 2 * NH helper warps of a level group (chunk c -> c mod 2NH)
+    constexpr int S = 2 * NH, CPW = (FEC + S - 1) / S;
     constexpr unsigned OFF_NEAR = 2 * NM, OFF_PN = 2 * (NM + NN);
     extern __shared__ __align__(16) unsigned char smem[];
     const int RING = a.ring_mask + 1;
-    const unsigned crank = cl_rank(), peer = crank ^ 1u;
+    const unsigned crank = cl_rank(), peer = 0u;   // helpers talk to the owner (rank 0)
     const bool owner = crank == 0;
     // role-specific staging (the helper's warps finish out of order, so it
     // keeps more rows in flight)
     const int lgc = owner ? a.lg_ch : a.lg_chh;
     const int ch = 1 << lgc;
     const unsigned ring_base = smem_u32(smem);                         // RING + 16 entries
-    const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // 2 x RING entries (owner)
+    const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // 2 NH buffers of SB entries (owner)
+    const int SB = RING / NH;
     u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(3 * RING + 16) * 8);
     constexpr int nb = kMaxStageCL + 2 * kLB;   // stage | lvlbar | farbar
     const unsigned lvl_u32 = smem_u32(bars + kMaxStageCL), far_u32 = lvl_u32 + kLB * 8;
@@ -896,7 +900,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     const unsigned nbytes = owner ? (unsigned)ch * a.kpn * 2 : 0u, fbytes = owner ? 0u : (unsigned)ch * a.kpf * 2;
     const unsigned gbytes = owner ? (unsigned)ch * 8 : 0u, ubytes = owner ? (unsigned)ch * 4 : 0u;
     const unsigned sbytes = nbytes + fbytes + gbytes + ubytes;
-    const int b = blockIdx.x >> 1;
+    const int b = blockIdx.x / (NH + 1);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const T *gcol = reinterpret_cast<const T *>(a.gP) + (size_t)b * a.npad;
     const int32_t nchunks = (int32_t)(a.npad >> lgc);
@@ -975,15 +979,16 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         // far rows, halving the latency of a level's far sum; the owner adds
         // the two partial sums (sfar[0], sfar[1]).
         const int g = warp >> 1, hh = warp & 1;   // the two warps of a pair on different SMSPs
-        const unsigned sfar_h = sfar_base + (unsigned)(hh * RING) * 8u;
+        const int qi = ((int)crank - 1) * 2 + hh;   // this warp's chunk class (mod 2 NH)
+        const unsigned sfar_h = sfar_base + (unsigned)(qi * SB) * 8u;
         int32_t hcb = 0, hlo, hhi;   // level bounds of this warp's next 32 levels, in registers
         hlo = a.lvl_ptr[min(g + lane * kNWC, a.ell)];
         hhi = a.lvl_ptr[min(g + lane * kNWC + 1, a.ell)];
-        auto far_sum = [&](const uint4 (&w)[FEC], unsigned nf) -> T {
+        auto far_sum = [&](const uint4 (&w)[2 * CPW], unsigned nf) -> T {
             T acc = T(0);
 #pragma unroll
-            for (int j = 0; j < FEC / 2; j++) {
-                if ((unsigned)(2 * j + hh) >= nf) break;   // warp-uniform: the group's colour count
+            for (int j = 0; j < CPW; j++) {
+                if ((unsigned)(qi + S * j) >= nf) break;   // warp-uniform: the group's colour count
                 const unsigned ws[8] = {w[2 * j].x, w[2 * j].y, w[2 * j].z, w[2 * j].w,
                                         w[2 * j + 1].x, w[2 * j + 1].y, w[2 * j + 1].z, w[2 * j + 1].w};
                 T v[16];
@@ -1000,18 +1005,18 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             }
             return acc;
         };
-        auto load_row = [&](int32_t ee, uint4 (&w)[FEC], unsigned &c16) {
+        auto load_row = [&](int32_t ee, uint4 (&w)[2 * CPW], unsigned &c16) {
             const uint4 *rg = reinterpret_cast<const uint4 *>(a.Df + (size_t)ee * a.kpf);
             const int nq = a.fe / 8;   // the row's 16-byte words (fe <= 16 * FEC)
 #pragma unroll
-            for (int j = 0; j < FEC / 2; j++) {   // chunk 2j + hh = words 4j + 2hh, +1
-                const int q = 4 * j + 2 * hh;
+            for (int j = 0; j < CPW; j++) {   // chunk qi + S j = words 2 (qi + S j), +1
+                const int q = 2 * (qi + S * j);
                 w[2 * j] = q < nq ? __ldg(rg + q) : make_uint4(0, 0, 0, 0);
                 w[2 * j + 1] = q + 1 < nq ? __ldg(rg + q + 1) : make_uint4(0, 0, 0, 0);
             }
             c16 = __ldg(a.Df + (size_t)ee * a.kpf + a.fe);   // 16-entry chunks used by this row's group
         };
-        uint4 w0[FEC];
+        uint4 w0[2 * CPW];
         unsigned c0 = 0;
         for (int32_t L = g, i = 0; L < a.ell; L += kNWC, i++) {
             if (i - hcb == 32) {
@@ -1088,15 +1093,15 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         t1b = clock64();
                     }
                 }
-                if (e0 < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e0 & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+                if (e0 < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e0 & (SB - 1)) * 8u, peer), df_bits<T>(acc), fbar);
             }
             for (int32_t base = lo + 32; base < hi; base += 32) {   // wide levels: further passes
                 const int32_t e = base + lane;
-                uint4 w1[FEC];
+                uint4 w1[2 * CPW];
                 unsigned c1;
                 load_row(e < hi ? e : base, w1, c1);
                 const T acc = (a.skip_far & 1) ? T(0) : far_sum(w1, __reduce_max_sync(0xffffffffu, c1));
-                if (e < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e & a.ring_mask) * 8u, peer), df_bits<T>(acc), fbar);
+                if (e < hi) cl_st_async64(cl_mapa(sfar_h + (unsigned)(e & (SB - 1)) * 8u, peer), df_bits<T>(acc), fbar);
             }
             if (PROF && b == 0 && lane == 0 && hh == 0) {
                 const long long t2 = PROF ? clock64() : 0;
@@ -1132,7 +1137,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
             const int32_t np = min((hi - lo + 31) >> 5, kNP);
             // arm this level's far-sum phase (the helper's st.async land on it);
             // phase L-16 completed when this warp consumed level L-16
-            if (lane == 0) cl_expect(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, 16u * (unsigned)(hi - lo));
+            if (lane == 0) cl_expect(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, 16u * NH * (unsigned)(hi - lo));
             while (staged < hi) staged = df_acq(ctrl);
             auto level = [&](auto npx) {
                 constexpr int NPX = decltype(npx)::value;
@@ -1183,8 +1188,9 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
 #pragma unroll
                 for (int p = 0; p < NPX; p++)
                     if (act(p))
-                        sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)((lo + 32 * p + lane) & a.ring_mask) * 8u)) +
-                                 bits_to<T>(df_lds64(sfar_base + (unsigned)(RING + ((lo + 32 * p + lane) & a.ring_mask)) * 8u));
+#pragma unroll
+                        for (int k2 = 0; k2 < 2 * NH; k2++)
+                            sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + ((lo + 32 * p + lane) & (SB - 1))) * 8u));
                 unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
                 df_pin(lvl_addr);
                 T gs[NPX], Fx[NPX];
@@ -1241,14 +1247,18 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         int32_t u1;
                         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + nbytes + gbytes + off * 4));
                         const unsigned p16 = lds32u(row + OFF_PN) & 0xffffu;
-                        const T s1 = bits_to<T>(df_lds64(sfar_base + (unsigned)(ee & a.ring_mask) * 8u)) +
-                                     bits_to<T>(df_lds64(sfar_base + (unsigned)(RING + (ee & a.ring_mask)) * 8u)) +
+                        T sf1 = T(0);
+#pragma unroll
+                        for (int k2 = 0; k2 < 2 * NH; k2++)
+                            sf1 += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + (ee & (SB - 1))) * 8u));
+                        const T s1 = sf1 +
                                      df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
                         const T F1 = g1 - s1;
                         if (e < hi) {
                             const unsigned sl = ring_base + (unsigned)(e & a.ring_mask) * 8u;
                             asm volatile("st.shared.b64 [%0], %1;" ::"r"(sl), "l"(df_bits<T>(F1)) : "memory");
-                            cl_st_async64(cl_mapa(sl, peer), df_bits<T>(F1), cl_mapa(lvl_addr, peer));
+#pragma unroll
+                            for (unsigned r = 1; r <= NH; r++) cl_st_async64(cl_mapa(sl, r), df_bits<T>(F1), cl_mapa(lvl_addr, r));
                             f[(size_t)u1 * a.B + b] = F1 - bits_to<T>(df_lds64(ring_base + p16));
                         }
                     }
@@ -1264,10 +1274,13 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                 // forward F to the helper's ring: each store completes its bytes
                 // on the helper's lvlbar[L % kLB] (armed there with 8 * width)
                 {
-                    const unsigned rbar = cl_mapa(lvl_addr, peer);
 #pragma unroll
-                    for (int p = 0; p < NPX; p++)
-                        if (stp[p]) cl_st_async64(cl_mapa(sa[p], peer), df_bits<T>(Fx[p]), rbar);
+                    for (unsigned r = 1; r <= NH; r++) {
+                        const unsigned rbar = cl_mapa(lvl_addr, r);
+#pragma unroll
+                        for (int p = 0; p < NPX; p++)
+                            if (stp[p]) cl_st_async64(cl_mapa(sa[p], r), df_bits<T>(Fx[p]), rbar);
+                    }
                 }
 #pragma unroll
                 for (int p = 0; p < NPX; p++)
@@ -1292,12 +1305,15 @@ void ringcl_plan(RingDFPlan &R) {
     R.ch_h = R.ch;
     R.nstage_h = R.nstage;
     R.cl_ok = R.ok && R.fe <= 128 && ringcl_smem_bytes(R) <= kSmemCapDF;
+    R.nh_max = 2;   // two helpers: 4 far-sum buffers of RING / 2 entries (>= 9 level widths)
 }
 
 bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
 
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t B, cudaStream_t s) {
+                                  int dtype, const void *gP, void *f, int64_t B, int num_sms, cudaStream_t s) {
+    // two helper CTAs per column when three SMs per column fit one wave
+    const int nh = (3 * B <= num_sms && R.nh_max >= 2) ? 2 : 1;
     if (P.n == 0) return cudaSuccess;
     if (!ringcl_fits(R)) return cudaErrorInvalidConfiguration;
     RDFArgs a{};
@@ -1329,8 +1345,10 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     if (R.nn == NN && R.nm == NM && fec == FEC)                                                \
         fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, true>              \
                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC, true>)          \
-                    : (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC>                    \
-                                  : (void *)k_moeb_ringcl<double, NN, NM, FEC>);
+           : nh == 2 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, false, 2>         \
+                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC, false, 2>)     \
+                     : (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC>                   \
+                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC>);
 #define RCL_NM(NN, FEC) RCL_FN(NN, 16, FEC) RCL_FN(NN, 32, FEC)
 #define RCL_FE(FEC) RCL_NM(4, FEC) RCL_NM(8, FEC) RCL_NM(16, FEC)
     const int fec = R.fe <= 64 ? 4 : R.fe <= 96 ? 6 : 8;   // chunks per row, split by parity
@@ -1342,13 +1360,14 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * B));
+    const int cdim = R.prof ? 2 : nh + 1;   // the instrumented build is the 1-helper kernel
+    cfg.gridDim = dim3((unsigned)(cdim * B));
     cfg.blockDim = dim3(32 * kNWH);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = (unsigned)cdim;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
