@@ -662,6 +662,11 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         }
         return POSET_OK;
     }
+    if (!strcmp(key, "ringcl_helpers")) {   // RINGCL helper CTAs per column (tuning; 0 = auto)
+        if (value < 0 || value > 3) return fail(POSET_EINVAL, "ringcl_helpers is 0..3");
+        h->rdf.nh_force = (int32_t)value;
+        return POSET_OK;
+    }
     if (!strcmp(key, "ring_debug")) {   // timing experiments only (bit 0: results NOT valid,
                                          // bit 3: instrumented RINGDF -> poset_debug_read)
         h->ring.debug = (int32_t)(value & 1);

@@ -135,7 +135,8 @@ struct RingDFPlan {
     int32_t wmax = 0;                 // widest level
     int32_t ch_h = 0, nstage_h = 0;   // RINGCL helper staging
     bool cl_ok = false;               // RINGCL fits shared memory
-    int32_t nh_max = 1;               // RINGCL helper CTAs per column (1 or 2)
+    int32_t nh_max = 1;               // RINGCL helper CTAs per column (1..3) the buffers allow
+    int32_t nh_force = 0;             // RINGCL helpers forced (option ringcl_helpers; 0 = auto)
     int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only

@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     const int ch = 1 << lgc;
     const unsigned ring_base = smem_u32(smem);                         // RING + 16 entries
     const unsigned sfar_base = ring_base + (unsigned)(RING + 16) * 8;   // 2 NH buffers of SB entries (owner)
-    const int SB = RING / NH;
+    const int SB = RING >> (NH == 1 ? 0 : NH == 2 ? 1 : 2);   // 2 NH buffers fit in 2 RING entries
     u64 *bars = reinterpret_cast<u64 *>(smem + (size_t)(3 * RING + 16) * 8);
     constexpr int nb = kMaxStageCL + 2 * kLB;   // stage | lvlbar | farbar
     const unsigned lvl_u32 = smem_u32(bars + kMaxStageCL), far_u32 = lvl_u32 + kLB * 8;
@@ -1305,7 +1305,11 @@ void ringcl_plan(RingDFPlan &R) {
     R.ch_h = R.ch;
     R.nstage_h = R.nstage;
     R.cl_ok = R.ok && R.fe <= 128 && ringcl_smem_bytes(R) <= kSmemCapDF;
-    R.nh_max = 2;   // two helpers: 4 far-sum buffers of RING / 2 entries (>= 9 level widths)
+    // helper CTAs: 2 NH far-sum buffers of RING >> {0,1,2} entries, each
+    // holding >= 10 level widths (the helpers run <= 8 levels ahead)
+    R.nh_max = 1;
+    if ((R.ring >> 1) >= 10 * R.wmax) R.nh_max = 2;
+    if ((R.ring >> 2) >= 10 * R.wmax) R.nh_max = 3;
 }
 
 bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
@@ -1313,7 +1317,11 @@ bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
                                   int dtype, const void *gP, void *f, int64_t B, int num_sms, cudaStream_t s) {
     // two helper CTAs per column when three SMs per column fit one wave
-    const int nh = (3 * B <= num_sms && R.nh_max >= 2) ? 2 : 1;
+    // (measured on C5w: 1 helper 128.0 ms, 2 helpers 100.4, 3 helpers 103.7;
+    // three stay available through the ringcl_helpers option)
+    int nh = 1;
+    if (R.nh_max >= 2 && 3 * B <= num_sms) nh = 2;
+    if (R.nh_force > 0) nh = std::min(R.nh_force, R.nh_max);   // tuning option ringcl_helpers
     if (P.n == 0) return cudaSuccess;
     if (!ringcl_fits(R)) return cudaErrorInvalidConfiguration;
     RDFArgs a{};
@@ -1345,6 +1353,8 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     if (R.nn == NN && R.nm == NM && fec == FEC)                                                \
         fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, true>              \
                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC, true>)          \
+           : nh == 3 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, false, 3>         \
+                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC, false, 3>)     \
            : nh == 2 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, false, 2>         \
                                    : (void *)k_moeb_ringcl<double, NN, NM, FEC, false, 2>)     \
                      : (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC>                   \

@@ -32,6 +32,10 @@ def clk(kern):
 res["ringdf_clk"] = clk(pz.MOEB_RINGDF)
 if info["ringdf"] & 2:
     res["ringcl_clk"] = clk(pz.MOEB_RINGCL)
+    for nh in (1, 2, 3):
+        P.set_option("ringcl_helpers", nh)
+        res[f"ringcl_h{nh}_clk"] = clk(pz.MOEB_RINGCL)
+    P.set_option("ringcl_helpers", 0)
     P.set_option("ring_debug", 8)
     P.moebius(g, out=y); torch.cuda.synchronize()
     d = P.debug_read()
