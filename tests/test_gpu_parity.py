@@ -228,6 +228,10 @@ def test_ring_schedule_selection_and_limits():
         assert (gpu_moebius(P, h, pz.MOEB_RINGDF) == want).all(), B
         assert info["ringdf"] & 2
         assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), B
+        for nh in (1, 2, 3):   # helper CTAs per column (cluster of nh + 1)
+            P.set_option("ringcl_helpers", nh)
+            assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), (B, nh)
+        P.set_option("ringcl_helpers", 0)
         for lpe in (1, 2, 4, 8):
             P.set_option("ring_lpe", lpe)
             assert (gpu_moebius(P, h, pz.MOEB_RING) == want).all(), (B, lpe)
