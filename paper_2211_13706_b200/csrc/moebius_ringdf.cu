@@ -803,22 +803,25 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
 }
 
 // ---------------------------------------------------------------------------
-// Schedule RINGCL: RINGDF over a CTA pair (cluster of 2) per column, so that
-// a second SM's shared-memory pipe and issue slots take the far sums.
+// Schedule RINGCL: RINGDF over a thread-block cluster of 1 + NH CTAs per
+// column (NH = 1..3 helpers; 2 by default), so that other SMs' shared-memory
+// pipes and issue slots take the far sums.
 //   owner  (cluster rank 0): the level pipeline of RINGDF -- rows (near
 //          table), mid sums, the near wait, F into its ring -- but the far
-//          sum of each element comes from the helper through DSMEM (two
-//          partial sums in sfar[0..1], landing on farbar[L % kLB], armed by
-//          the owner with 16 bytes per element).  After publishing level L
-//          locally it forwards F to the helper's ring with st.async, each
-//          store completing 8 bytes on the helper's lvlbar[L % kLB].
-//   helper (cluster rank 1): 16 warps; warps g and g+8 own the levels
-//          L = g (mod 8) and the even / odd 16-entry chunks of their far rows.
-//          A warp arms lvlbar[L % kLB] (8 bytes per element), loads its
-//          level's far-row words from global memory into registers (their
-//          latency hides behind the wait), waits for the owner's levels
-//          L-14 .. L-7 (they are published out of order; older ones it saw at
-//          level L-8), sums and st.async's its partial sums to the owner.
+//          sum of each element comes from the helpers through DSMEM (2 NH
+//          partial sums in the sfar buffers, landing on farbar[L % kLB],
+//          armed by the owner with 16 NH bytes per element).  After
+//          publishing level L locally it forwards F to every helper's ring
+//          with st.async, each store completing 8 bytes on that helper's
+//          lvlbar[L % kLB].
+//   helper (cluster ranks 1..NH): 16 warps; warps 2g and 2g+1 own the
+//          levels L = g (mod 8) and the 16-entry far chunks c = qi (mod 2 NH)
+//          of their rows (qi = 2 (rank - 1) + warp parity).  A warp arms
+//          lvlbar[L % kLB] (8 bytes per element), loads its level's far-row
+//          words from global memory into registers (their latency hides
+//          behind the wait), waits for the owner's levels L-14 .. L-7 (they
+//          are published out of order; older ones it saw at level L-8), sums
+//          and st.async's its partial sums to the owner.
 // Slack: the far sum of level L is needed when level L-1 completes, i.e.
 // 6 level times after level L-7 completed (a DSMEM round trip is ~320
 // cycles).  Waits are CTA-scope try_waits: the bytes are made visible by the
@@ -973,11 +976,10 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         // before the wait for the owner's levels (their latency hides behind
         // it); no staging, so no coupling between the out-of-order helper
         // warps and a stage ring.
-        // Two warps per level (kNWH = 16): warp (g, hh) = (warp / 2, warp % 2)
-        // (the pair on different SM sub-partitions) owns the levels
-        // L = g (mod 8) and the chunks c = hh (mod 2) of their
-        // far rows, halving the latency of a level's far sum; the owner adds
-        // the two partial sums (sfar[0], sfar[1]).
+        // Two warps per level group and helper (kNWH = 16): warp (g, hh) =
+        // (warp / 2, warp % 2) (the pair on different SM sub-partitions) owns
+        // the levels L = g (mod 8) and the chunks c = qi (mod 2 NH) of their
+        // far rows; the owner adds the 2 NH partial sums.
         const int g = warp >> 1, hh = warp & 1;   // the two warps of a pair on different SMSPs
         const int qi = ((int)crank - 1) * 2 + hh;   // this warp's chunk class (mod 2 NH)
         const unsigned sfar_h = sfar_base + (unsigned)(qi * SB) * 8u;
