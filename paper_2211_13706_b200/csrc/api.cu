@@ -432,9 +432,15 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
             CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
         }
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        if (which == MOEB_RINGCL)
-            CK(launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s));
-        else
+        if (which == MOEB_RINGCL) {
+            cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s);
+            if (ce == cudaErrorInvalidConfiguration && h->moeb_opt == MOEB_AUTO) {   // no cluster fits: RINGDF
+                cudaGetLastError();
+                h->info.moebius_kernel = MOEB_RINGDF;
+                ce = launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s);
+            }
+            CK(ce);
+        } else
             CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
         return POSET_OK;
     }

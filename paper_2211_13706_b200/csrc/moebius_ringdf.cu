@@ -1384,6 +1384,18 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // a cluster that cannot be placed at all (fewer SMs per GPC, MIG, ...)
+    // falls back to fewer helpers before launching
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters == 0) {
+        cudaGetLastError();
+        if (nh > 1 && !R.prof) {
+            RingDFPlan R2 = R;
+            R2.nh_force = nh - 1;
+            return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s);
+        }
+        return cudaErrorInvalidConfiguration;
+    }
     void *args[] = {&a};
     launches_add(1);
     return cudaLaunchKernelExC(&cfg, fn, args);
