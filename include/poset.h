@@ -27,10 +27,22 @@
  *  Streams    `stream` is a cudaStream_t passed as void* (NULL = legacy
  *             default stream).  Compute calls are asynchronous and
  *             stream-ordered; setup is synchronous.
- *  Threads    a handle is not re-entrant: serialise calls per handle.
+ *  Threads    a handle is not re-entrant: serialise calls per handle (host
+ *             side).  Calls on DIFFERENT streams are ordered by the library:
+ *             each call records an event on its stream and a call on another
+ *             stream waits on it first, because all calls share the handle's
+ *             scratch buffers.  A host result is valid once `stream` has
+ *             synchronised (poset_sync).
  *  Errors     return codes, never exceptions; poset_last_error() gives the
- *             calling thread's last message.  CUDA failures are sticky in the
- *             handle (POSET_ECUDA).
+ *             calling thread's last message.  CUDA faults inside a kernel
+ *             (illegal address, launch failure, ...) are sticky in the handle
+ *             (POSET_ECUDA); recoverable CUDA errors (a device allocation that
+ *             does not fit -> POSET_ENOMEM, a launch that cannot be placed) are
+ *             returned once and cleared.
+ *  Alignment  split-phase entry points (poset_scan_slots .. poset_rank_to_user)
+ *             take device pointers only: [n][B] arrays 32-byte aligned, tail /
+ *             carry arrays 8-byte aligned; anything else is POSET_EINVAL.
+ *             poset_zeta / poset_moebius accept any pointer (they stage).
  *
  * Internal layout: elements are ranked in level order
  * (Alg. 6 antichains, bottom-up, ties by user id); chains are
@@ -59,7 +71,7 @@ typedef enum {
     POSET_ENOTCHAIN = 4,      /* injected chain with consecutive incomparable elements  */
     POSET_ENOTPARTITION = 5,  /* injected chains do not partition 0..n-1                */
     POSET_ETOOBIG = 6,        /* dense n*k*4-byte table + buffers exceed free device memory      */
-    POSET_ENOMEM = 7,         /* host allocation failed                                          */
+    POSET_ENOMEM = 7,         /* host allocation, or a device scratch allocation, failed (not sticky) */
     POSET_ECUDA = 8           /* CUDA error (no device, launch failure, ...) -- sticky           */
 } poset_status;
 
@@ -251,6 +263,10 @@ poset_status poset_export_mtable(poset_t h, int32_t *out);
  * [0] row data + ring loads + tree, [1] lane reduction, [2] tail,
  * [3] next-level prefetch, [4] barrier, [5] levels). */
 poset_status poset_debug_read(poset_t h, int64_t *out8);
+
+/* poset_sync -- cudaStreamSynchronize(stream) on the handle's device (host
+ * results of poset_zeta / poset_moebius are valid after it). */
+poset_status poset_sync(poset_t h, void *stream);
 
 void poset_destroy(poset_t h);
 const char *poset_strerror(poset_status s);

@@ -82,6 +82,7 @@ _sig("poset_destroy", [_vp], None)
 _sig("poset_strerror", [ctypes.c_int], ctypes.c_char_p)
 _sig("poset_last_error", [], ctypes.c_char_p)
 _sig("poset_abi_version", [], ctypes.c_int)
+_sig("poset_sync", [_vp, _vp])
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "ESELFLOOP", 3: "ECYCLE", 4: "ENOTCHAIN", 5: "ENOTPARTITION",
           6: "ETOOBIG", 7: "ENOMEM", 8: "ECUDA"}
@@ -250,7 +251,14 @@ class Poset:
         dt = _dtype_code(x)
         if _dtype_code(out) != dt:
             raise TypeError("input and output dtypes differ")
-        _check(fn(self._h, _ptr(x), _ptr(out), batch, dt, _stream_ptr(stream, x)))
+        for t in (x, out):
+            if not isinstance(t, np.ndarray) and t.is_cuda and t.device.index != self.device:
+                raise ValueError(f"tensor on {t.device}, poset on cuda:{self.device}")
+        sp = _stream_ptr(stream, x)
+        _check(fn(self._h, _ptr(x), _ptr(out), batch, dt, sp))
+        if isinstance(out, np.ndarray) or not out.is_cuda:
+            # a host result is complete only once the staging copy has landed
+            _check(lib.poset_sync(self._h, sp))
         return out
 
     def zeta(self, f, out=None, stream=None):

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -30,6 +31,13 @@ struct poset_s {
     poset_info info{};
     int moeb_opt = MOEB_AUTO;
     cudaError_t sticky = cudaSuccess;
+    // cross-stream ordering of calls on one handle: every call records
+    // done_ev on its stream; a call on a different stream first waits on it,
+    // so the handle's scratch (F, scan, partial, staging) is never shared by
+    // two calls in flight
+    cudaEvent_t done_ev = nullptr;
+    cudaStream_t last_s = nullptr;
+    bool used = false;
     // device residency
     int32_t *d_rank_user = nullptr, *d_slot = nullptr, *d_chain = nullptr, *d_lvl = nullptr;
     int32_t *d_child = nullptr, *d_slot_user = nullptr, *d_M = nullptr;
@@ -74,12 +82,34 @@ struct poset_s {
     }
 };
 
+// Errors that leave the CUDA context unusable (a fault inside a kernel) are
+// sticky in the handle; recoverable ones (an allocation that does not fit, a
+// launch configuration that cannot be placed, a bad argument) are returned
+// once and cleared from the runtime's last-error slot so they do not leak into
+// the next call on this or another handle.
+static bool fatal_cuda_error(cudaError_t e) {
+    switch (e) {
+        case cudaErrorIllegalAddress: case cudaErrorLaunchFailure: case cudaErrorHardwareStackError:
+        case cudaErrorIllegalInstruction: case cudaErrorMisalignedAddress:
+        case cudaErrorInvalidAddressSpace: case cudaErrorInvalidPc: case cudaErrorLaunchTimeout:
+        case cudaErrorECCUncorrectable: case cudaErrorAssert: case cudaErrorUnknown:
+            return true;
+        default:
+            return false;
+    }
+}
+
 #define CK(expr)                                                                              \
     do {                                                                                      \
         cudaError_t _e = (expr);                                                              \
         if (_e != cudaSuccess) {                                                              \
-            if (h) h->sticky = _e;                                                            \
-            return fail(POSET_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+            if (fatal_cuda_error(_e)) {                                                       \
+                if (h) h->sticky = _e;                                                        \
+            } else {                                                                          \
+                cudaGetLastError();                                                           \
+            }                                                                                 \
+            return fail(_e == cudaErrorMemoryAllocation ? POSET_ENOMEM : POSET_ECUDA,         \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                  \
         }                                                                                     \
     } while (0)
 
@@ -90,6 +120,7 @@ static void free_all(poset_s *h) {
     cudaSetDevice(h->device);
     for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
+    if (h->done_ev) cudaEventDestroy(h->done_ev);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
                     h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
@@ -133,6 +164,7 @@ static poset_status finish_setup(poset_s *h) {
     CK(upload(&h->d_child_ptr, H.child_ptr));
     CK(upload(&h->d_child, H.child));
     CK(upload(&h->d_slot_user, H.slot_user));
+    CK(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
     CK(cudaMalloc((void **)&h->d_bar, 64));
     CK(cudaMalloc((void **)&h->d_count, 64));
     CK(cudaMalloc((void **)&h->d_M, std::max<size_t>(table, 4)));
@@ -338,6 +370,23 @@ static bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// 32-byte aligned device memory: what the split-phase kernels' 256-bit
+// vector loads and stores need (the transforms stage anything else).
+static bool dev_aligned(const void *p) { return is_device_ptr(p) && ((uintptr_t)p % 32) == 0; }
+
+static poset_status begin_call(poset_s *h, cudaStream_t s) {
+    if (h->used && s != h->last_s) CK(cudaStreamWaitEvent(s, h->done_ev, 0));
+    return POSET_OK;
+}
+
+static poset_status end_call(poset_s *h, cudaStream_t s, poset_status st) {
+    if (st != POSET_OK) return st;
+    CK(cudaEventRecord(h->done_ev, s));
+    h->last_s = s;
+    h->used = true;
+    return POSET_OK;
+}
+
 static poset_status ensure_F(poset_s *h, int64_t batch, cudaStream_t s) {
     size_t need = (size_t)(h->H.n + 1) * batch * 8;
     poset_status st = grow(h, &h->d_F, &h->F_bytes, need);
@@ -520,7 +569,9 @@ poset_status poset_zeta(poset_t h, const void *f, void *g, int64_t batch, poset_
     poset_status st = check_call(h, f, g, batch, dt, "poset_zeta");
     if (st || h->H.n == 0) return st;
     CK(cudaSetDevice(h->device));
-    return run_staged(h, zeta_dev, f, g, batch, dt, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    return end_call(h, s, run_staged(h, zeta_dev, f, g, batch, dt, s));
 }
 
 poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, poset_dtype dt,
@@ -528,7 +579,25 @@ poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, pos
     poset_status st = check_call(h, g, f, batch, dt, "poset_moebius");
     if (st || h->H.n == 0) return st;
     CK(cudaSetDevice(h->device));
-    return run_staged(h, moebius_dev, g, f, batch, dt, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    return end_call(h, s, run_staged(h, moebius_dev, g, f, batch, dt, s));
+}
+
+// Split phases: caller pointers go straight to the kernels (no staging), so
+// they must be device memory: [n][B] arrays 32-byte aligned (256-bit vector
+// accesses), the small tail / carry arrays 8-byte aligned (scalar accesses).
+static poset_status check_split(const char *fn, std::initializer_list<const void *> arrays,
+                                std::initializer_list<const void *> small = {}) {
+    for (const void *p : arrays)
+        if (p && !dev_aligned(p))
+            return fail(POSET_EINVAL, std::string(fn) + ": [n][B] arrays must be 32-byte aligned "
+                                                        "device pointers (split phases do not stage)");
+    for (const void *p : small)
+        if (p && !(is_device_ptr(p) && (uintptr_t)p % 8 == 0))
+            return fail(POSET_EINVAL, std::string(fn) + ": tail / carry must be 8-byte aligned "
+                                                        "device pointers");
+    return POSET_OK;
 }
 
 poset_status poset_scan_slots(poset_t h, const void *f, void *F, void *tail, int64_t lo, int64_t hi,
@@ -537,10 +606,13 @@ poset_status poset_scan_slots(poset_t h, const void *f, void *F, void *tail, int
     if (st) return st;
     if (lo < 0 || hi > h->H.n || lo > hi || !tail) return fail(POSET_EINVAL, "poset_scan_slots: bad range");
     CK(cudaSetDevice(h->device));
+    if ((st = check_split("poset_scan_slots", {f, F}, {tail}))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
     st = grow(h, &h->d_scan, &h->scan_bytes, scan_scratch_bytes(hi - lo, batch));
     if (st) return st;
-    CK(launch_scan(h->dev(), dt, f, F, lo, hi, batch, h->d_scan, tail, (cudaStream_t)stream));
-    return POSET_OK;
+    CK(launch_scan(h->dev(), dt, f, F, lo, hi, batch, h->d_scan, tail, s));
+    return end_call(h, s, POSET_OK);
 }
 
 poset_status poset_scan_carry(poset_t h, void *F, const void *carry, int64_t lo, int64_t hi,
@@ -553,8 +625,11 @@ poset_status poset_scan_carry(poset_t h, void *F, const void *carry, int64_t lo,
     auto itr = std::lower_bound(off.begin(), off.end() - 1, (int32_t)lo);
     int64_t end = itr == off.end() - 1 ? hi : std::min<int64_t>(hi, *itr);
     CK(cudaSetDevice(h->device));
-    CK(launch_scan_carry(h->dev(), dt, F, carry, lo, end, batch, (cudaStream_t)stream));
-    return POSET_OK;
+    if ((st = check_split("poset_scan_carry", {F}, {carry}))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    CK(launch_scan_carry(h->dev(), dt, F, carry, lo, end, batch, s));
+    return end_call(h, s, POSET_OK);
 }
 
 poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t lo, int64_t hi,
@@ -563,18 +638,20 @@ poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t l
     if (st) return st;
     if (lo < 0 || hi > h->H.n || lo > hi) return fail(POSET_EINVAL, "poset_gather_rows: bad range");
     CK(cudaSetDevice(h->device));
+    if ((st = check_split("poset_gather_rows", {F, g_rank}))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
     if (h->zeta_csr) {
-        CK(launch_gather_csr(h->dev(), h->csr, dt, F, g_rank, lo, hi, batch, 1, (cudaStream_t)stream));
-        return POSET_OK;
+        CK(launch_gather_csr(h->dev(), h->csr, dt, F, g_rank, lo, hi, batch, 1, s));
+        return end_call(h, s, POSET_OK);
     }
     size_t pb = gather_partial_bytes(h->dev(), hi - lo, batch, h->num_sms);
     if (pb) {
         st = grow(h, &h->d_part, &h->part_bytes, pb);
         if (st) return st;
     }
-    CK(launch_gather(h->dev(), dt, F, g_rank, lo, hi, batch, 1, pb ? h->d_part : nullptr, h->num_sms,
-                     (cudaStream_t)stream));
-    return POSET_OK;
+    CK(launch_gather(h->dev(), dt, F, g_rank, lo, hi, batch, 1, pb ? h->d_part : nullptr, h->num_sms, s));
+    return end_call(h, s, POSET_OK);
 }
 
 poset_status poset_combine_tails(poset_t h, const void *tails_all, int64_t world, int64_t rank,
@@ -583,8 +660,11 @@ poset_status poset_combine_tails(poset_t h, const void *tails_all, int64_t world
     if (st) return st;
     if (world <= 0 || rank < 0 || rank >= world) return fail(POSET_EINVAL, "poset_combine_tails: bad rank");
     CK(cudaSetDevice(h->device));
-    CK(launch_combine_tails(dt, tails_all, world, rank, carry_out, batch, (cudaStream_t)stream));
-    return POSET_OK;
+    if ((st = check_split("poset_combine_tails", {}, {tails_all, carry_out}))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    CK(launch_combine_tails(dt, tails_all, world, rank, carry_out, batch, s));
+    return end_call(h, s, POSET_OK);
 }
 
 poset_status poset_rank_to_user(poset_t h, const void *g_rank, void *g_user, int64_t batch,
@@ -592,8 +672,11 @@ poset_status poset_rank_to_user(poset_t h, const void *g_rank, void *g_user, int
     poset_status st = check_call(h, g_rank, g_user, batch, dt, "poset_rank_to_user");
     if (st) return st;
     CK(cudaSetDevice(h->device));
-    CK(launch_rank_to_user(h->dev(), dt, g_rank, g_user, batch, (cudaStream_t)stream));
-    return POSET_OK;
+    if ((st = check_split("poset_rank_to_user", {g_rank, g_user}))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    CK(launch_rank_to_user(h->dev(), dt, g_rank, g_user, batch, s));
+    return end_call(h, s, POSET_OK);
 }
 
 poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
@@ -752,6 +835,13 @@ poset_status poset_export_mtable(poset_t h, int32_t *out) {
             int32_t v = M[(size_t)j * H.n + r];
             out[(size_t)H.rank_user[r] * H.k + j] = v == H.n ? -1 : v - H.chain_off[j];
         }
+    return POSET_OK;
+}
+
+poset_status poset_sync(poset_t h, void *stream) {
+    if (!h) return fail(POSET_EINVAL, "poset_sync: null handle");
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
     return POSET_OK;
 }
 

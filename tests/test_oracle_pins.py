@@ -13,7 +13,7 @@ import pytest
 
 from conftest import assert_fp64_close, load_facts, load_matrix
 from oracle import brute
-from oracle.chain import ChainOracle
+from oracle.chain import ChainOracle, zeta_sampled_edges
 import workloads as W
 
 facts = load_facts()
@@ -334,3 +334,37 @@ def test_errors():
         ChainOracle(12, *W.paper_example_edges(), chains=[[2, 3]] + [[v] for v in range(12) if v not in (2, 3)])
     with pytest.raises(brute.CycleError):
         brute.downsets(2, np.array([0, 1]), np.array([1, 0]))
+
+
+def _edge_sample_cases():
+    s, d = W.window_dag(1200, 2, 64, 3, forced=True)
+    yield "window_w", 1200, s, d
+    s, d = W.window_dag(900, 3, 50, 1)
+    yield "window_lit", 900, s, d
+    s, d = W.layered_dag(6, 64, 3, 2, forced=True)
+    yield "layered", 6 * 64, s, d
+    s, d = W.boolean_lattice(8)
+    yield "bool8", 256, s, d
+    # duplicate edges (each edge twice, shuffled) and an isolated vertex
+    s, d = W.window_dag(700, 2, 30, 5)
+    rng = np.random.default_rng(9)
+    perm = rng.permutation(2 * s.shape[0])
+    yield "dups", 701, np.concatenate([s, s])[perm], np.concatenate([d, d])[perm]
+
+
+@pytest.mark.parametrize("case", list(_edge_sample_cases()), ids=lambda c: c[0])
+def test_zeta_sampled_edges_is_pinned_to_O1(case):
+    """The DFS checker used at full size (oracle_zeta_sampled_edges) against
+    the O1 closure sums, Eq. inv-formula: int64 bit-exact in Z/2^64,
+    fp64 within the tolerance, and its Σ|f| scale equal to O1's zeta(|f|)."""
+    name, n, src, dst = case
+    rng = np.random.default_rng(1)
+    xs = np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, 40)]))
+    fi = W.int_values(n, 3, -10**18, 10**18, seed=4)          # wraps in Z/2^64
+    gi, none = zeta_sampled_edges(n, src, dst, fi, xs)
+    assert none is None
+    assert (gi == brute.zeta(n, src, dst, fi)[xs]).all()
+    ff = W.normal_values(n, 2, seed=5)
+    gf, ab = zeta_sampled_edges(n, src, dst, ff, xs)
+    assert_fp64_close(gf, brute.zeta(n, src, dst, ff)[xs], brute.zeta_abs(n, src, dst, ff)[xs])
+    np.testing.assert_allclose(ab, brute.zeta_abs(n, src, dst, ff)[xs], rtol=1e-12)
