@@ -53,10 +53,14 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--moebius-kernel", default="auto", choices=MOEB_NAMES)
     ap.add_argument("--gather-variant", type=int, default=0, help="dense gather kernel for B%%32==0 (tuning)")
+    ap.add_argument("--gather-pi-cfg", type=int, default=0, help="gather-order kernel configuration (tuning)")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-provenance", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="oracle prefix size")
     return ap.parse_args()
 
@@ -129,8 +133,19 @@ def dist_init():
     return world, rank, local
 
 
+def survey_bytes(n, k, B, info=None):
+    """SURVEY §8(d) algorithmic bytes per transform CALL: 4·n·k index
+    (4·nnz for the sparse table) + 32·n·B (f read, F written, F read once,
+    g written).  The roofline's `achieved` uses these for the transform whose
+    kernel dominates; the per-kernel models below split them by kernel."""
+    idx = 4 * n * k
+    if info is not None and info.get("zeta_sparse"):
+        idx = 4 * info["nnz"]
+    return idx + 32 * n * B
+
+
 def alg_bytes(n, k, B, info=None):
-    """Algorithmic bytes per launch of each phase."""
+    """Each kernel's own algorithmic bytes per launch."""
     d = {
         "scan": 16 * n * B + 4 * n,                 # f read, F write, slot->user
         "gather": 4 * n * k + 16 * n * B + 4 * n,   # index stream, F read once, g write
@@ -153,53 +168,82 @@ def alg_bytes(n, k, B, info=None):
     return d
 
 
-def oracle_sample(wl, B, n_sample, dtype):
-    """Time the CPU oracle O2 (Algs. 3 + 4, single thread) on the down-closed
-    prefix of the workload's first n_sample vertices (generator ids are
-    bottom-up, so the prefix is itself a poset of the same family)."""
-    import numpy as np
+def ncu_traffic(config, phase):
+    """DRAM bytes (read + write) per launch of the phase's kernel from the
+    committed ncu --set full capture summary (profiles/ncu_traffic.json,
+    written by scripts/profile_summaries.py from a .ncu-rep of this bench);
+    (None, reason) when there is no capture for this config and phase."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(tpath))
+        ent = d.get(config, {}).get(phase)
+        if isinstance(ent, dict):
+            return ent.get("bytes"), f"profiles/ncu_traffic.json ({ent.get('capture', '?')})"
+        if ent is not None:
+            return ent, "profiles/ncu_traffic.json"
+    except Exception:
+        pass
+    return None, "no ncu capture for this config/phase"
+
+
+def oracle_prefix(wl, B, n_sample, dtype):
+    """The CPU oracle O2 on the down-closed prefix of the workload's first
+    n_sample vertices (generator ids are bottom-up, so the prefix is itself a
+    poset of the same family) and its input f."""
     import workloads as W
     from oracle.chain import ChainOracle
     m = wl.src < n_sample
-    src, dst = wl.src[m], wl.dst[m]
-    O = ChainOracle(n_sample, src, dst)
-    if dtype == "i64":
-        f = W.int_values(n_sample, B, -1000, 1000, seed=1)
-    else:
-        f = W.normal_values(n_sample, B, seed=1)
+    O = ChainOracle(n_sample, wl.src[m], wl.dst[m])
+    f = (W.int_values(n_sample, B, -1000, 1000, seed=1) if dtype == "i64"
+         else W.normal_values(n_sample, B, seed=1))
+    return O, f
+
+
+def oracle_time(O, f, parallel):
+    """Seconds of one zeta + one Möbius (Algs. 3-4; `parallel`: the OpenMP
+    build -- chains / rows in parallel, Möbius by Alg. 5 antichain by
+    antichain, P:L692-705)."""
     t0 = time.perf_counter()
-    g = O.zeta(f)
-    O.moebius(g)
-    dt = time.perf_counter() - t0
-    return {"n": n_sample, "k": O.k, "nnz": O.nnz, "B": B, "seconds": dt,
-            "units": 2 * n_sample * O.k * B}
+    if parallel:
+        O.moebius_omp(O.zeta_omp(f))
+    else:
+        O.moebius(O.zeta(f))
+    return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the CPU oracle (OpenMP build, all host cores) on a
+    bounded prefix sample of the same workload, per step one zeta + one
+    Möbius; rank 0 only."""
     if rank != 0:
         return 0
     import workloads as W
+    from oracle.chain import threads
     wl = W.make_workload(args.config, args.scale, args.dtype, args.batch)
-    n_s = args.cpu_sample or min(wl.n, 400_000)
+    n_s = args.cpu_sample or min(wl.n, 1_000_000)
+    O, f = oracle_prefix(wl, wl.batch, n_s, wl.dtype)
     for _ in range(args.warmup):
-        oracle_sample(wl, wl.batch, n_s, wl.dtype)
-    tot_t, tot_u, last = 0.0, 0, None
-    for _ in range(args.steps):
-        r = oracle_sample(wl, wl.batch, n_s, wl.dtype)
-        tot_t += r["seconds"]
-        tot_u += r["units"]
-        last = r
-    value = tot_u / tot_t
-    sample = (f"prefix n={n_s} of {args.config} (k={last['k']}, nnz={last['nnz']}), B={wl.batch} "
-              f"{wl.dtype}, zeta+Möbius Algs. 3-4 single thread, setup excluded")
+        oracle_time(O, f, True)
+    tot_t = sum(oracle_time(O, f, True) for _ in range(args.steps))
+    units = 2 * n_s * O.k * wl.batch
+    value = units * args.steps / tot_t
+    sample = (f"prefix n={n_s} of {args.config} (k={O.k}, nnz={O.nnz}), B={wl.batch} {wl.dtype}, "
+              f"zeta+Möbius Algs. 3-5 OpenMP on {threads()} threads, setup excluded")
     line = {"impl": "reference", "metric": "zeta/Möbius n·k gathers/s", "value": value,
             "unit": "n·k·B gathers/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": wl.dtype, "data": "synthetic",
-            "config": {"workload": args.config, "n": wl.n, "batch_per_rank": wl.batch},
-            "cpu_baseline": {"value": value, "unit": "n·k·B gathers/s", "cores": 1,
-                             "kind": "oracle", "sample": sample},
+            "config": {"workload": args.config, "n": wl.n, "global_batch": wl.batch},
+            "cpu_baseline": {"value": value, "unit": "n·k·B gathers/s", "cores": threads(),
+                             "host_cores": host_cores(), "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "n·k·B gathers/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -225,24 +269,46 @@ def main():
     kern = MOEB_NAMES.index(args.moebius_kernel)
     P.set_option("moebius_kernel", kern)
     P.set_option("gather_variant", args.gather_variant)
+    P.set_option("gather_pi_cfg", args.gather_pi_cfg)
     if args.ring_debug:
         P.set_option("ring_debug", args.ring_debug)
-    f_host = wl.values(seed=1 + rank)
+    # strong scaling (default): BASELINE's global batch split over the ranks
+    # by columns (no data-path collective); a single function (batch < world)
+    # is row-sharded for zeta (NCCL all-gathers, dist.row_sharded_zeta) with
+    # Möbius on rank 0 (its dependency chain does not shard, north star).
+    # --scaling weak: every rank its own full batch.
+    from paper_2211_13706_b200 import dist as pdist
+    GB = wl.batch if args.scaling == "strong" else wl.batch * world
+    row_mode = args.scaling == "strong" and world > 1 and wl.batch < world
+    if args.scaling == "weak":
+        f_host = np.ascontiguousarray(wl.values(seed=1 + rank))
+        cols = (0, wl.batch)
+    else:
+        f_all = wl.values(seed=1)
+        cols = (0, wl.batch) if row_mode else pdist.column_shard(wl.batch, world, rank)
+        f_host = np.ascontiguousarray(f_all[:, cols[0]:cols[1]])
+        del f_all
+    B = f_host.shape[1]
     x = torch.from_numpy(f_host).cuda()
     g = torch.empty_like(x)
     y = torch.empty_like(x)
     n, k = info["n"], info["k"]
 
     def step():
-        P.zeta(x, out=g)
-        P.moebius(g, out=y)
+        if row_mode:
+            pdist.row_sharded_zeta(P, x, out=g)
+            if rank == 0:
+                P.moebius(g, out=y)
+        elif B > 0:
+            P.zeta(x, out=g)
+            P.moebius(g, out=y)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # correctness spot check of the timed computation (round trip)
     if wl.dtype == "i64":
-        ok = bool(torch.equal(y, x))
+        ok = bool(torch.equal(y, x)) if (rank == 0 or not row_mode) else None
     else:
         ok = None   # fp64 Möbius on deep posets is ill-conditioned (reading G8)
     P.set_option("profile", 1)
@@ -268,8 +334,8 @@ def main():
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    units_step = 2 * n * k * B
-    value = world * units_step * args.steps / (ms_max / 1e3)
+    units_step = 2 * n * k * GB            # whole job, all ranks
+    value = units_step * args.steps / (ms_max / 1e3)
 
     # per-kernel roofline (this rank; rank 0 reports)
     peak, peak_kind = peaks()
@@ -284,44 +350,49 @@ def main():
         gbs = ab[ph] / (per / 1e3) / 1e9
         kernels[ph] = {"kernel": KERNEL_NAMES[ph], "ms_per_call": per, "share": tms / ms,
                        "alg_bytes": ab[ph], "achieved_gbs": gbs, "frac": gbs / peak}
+    if not kernels:   # row-sharded zeta only on this rank (split phases are not phase-timed)
+        kernels = {"moebius_solve": {"kernel": KERNEL_NAMES["moebius_solve"], "ms_per_call": ms / args.steps,
+                                     "share": 1.0, "alg_bytes": ab["moebius_solve"], "achieved_gbs": 0.0,
+                                     "frac": 0.0}}
     dom = max(kernels, key=lambda p: kernels[p]["share"])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
-        except Exception:
-            traffic = None
-    roof = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "achieved": kernels[dom]["achieved_gbs"],
-            "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": kernels[dom]["frac"],
-            "traffic": traffic}
+    traffic, tsrc = ncu_traffic(args.config, dom)
+    sb = survey_bytes(n, k, B, info)
+    # the dominant kernel is one transform's kernel: §8(d) bytes of that call
+    dom_ms = kernels[dom]["ms_per_call"]
+    roof = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "alg_bytes": sb,
+            "alg_bytes_basis": "SURVEY §8(d): 4nk + 32nB per transform call",
+            "achieved": sb / (dom_ms / 1e3) / 1e9, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": sb / (dom_ms / 1e3) / 1e9 / peak,
+            "kernel_bytes": kernels[dom]["alg_bytes"], "kernel_frac": kernels[dom]["frac"],
+            "traffic": traffic, "traffic_source": tsrc}
     # the zeta gather is the kernel the north star's roofline target names
     zroof = None
     if "gather" in kernels:
-        zt = None
-        if os.path.exists(tpath):
-            try:
-                zt = json.load(open(tpath)).get(args.config, {}).get("gather")
-            except Exception:
-                zt = None
+        zt, zsrc = ncu_traffic(args.config, "gather")
         zroof = {"bound": "hbm", "kernel": kernels["gather"]["kernel"],
+                 "alg_bytes": kernels["gather"]["alg_bytes"],
+                 "alg_bytes_basis": "SURVEY §8(d) zeta bytes minus the scan's 16nB: 4nk + 16nB",
                  "achieved": kernels["gather"]["achieved_gbs"], "peak": peak, "peak_kind": peak_kind,
-                 "unit": "GB/s", "frac": kernels["gather"]["frac"], "traffic": zt}
+                 "unit": "GB/s", "frac": kernels["gather"]["frac"], "traffic": zt, "traffic_source": zsrc}
     if dom == "moebius_solve":
-        roof["note"] = (f"latency-bound triangular solve: {info['ell']} dependent levels, "
-                        f"{1e6 * kernels[dom]['ms_per_call'] / 1e3 / max(info['ell'], 1):.1f} µs per level")
+        P.set_option("compute_depth_u", 1)
+        du = P.info()["depth_u"]
+        roof["note"] = (f"latency-bound triangular solve: {info['ell']} dependent levels, D_U = {du}, "
+                        f"{1e3 * dom_ms / max(info['ell'], 1):.3f} µs per level")
         # the bound that matters for a dependent level sweep: per-level time
         # against the measured floor of one level hand-off between two warps
         # (mbarrier arrive -> try_wait wake, scripts/micro/handoff.cu: 91 cycles)
         mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
-        cyc = kernels[dom]["ms_per_call"] * 1e-3 * mhz * 1e6 / max(info["ell"], 1)
+        cyc = dom_ms * 1e-3 * mhz * 1e6 / max(info["ell"], 1)
         roof["latency"] = {"cycles_per_level": cyc, "floor_cycles_per_level": 91.0,
                            "floor": "two-warp mbarrier hand-off, measured (scripts/micro/handoff.cu)",
-                           "frac": 91.0 / cyc}
+                           "frac": 91.0 / cyc, "depth_u": du,
+                           "us_per_DU_step": 1e3 * dom_ms / max(du, 1),
+                           "cycles_per_DU_step": dom_ms * 1e-3 * mhz * 1e6 / max(du, 1)}
 
     # e2e: C-ABI with pinned host buffers, copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not row_mode:
         fp = torch.from_numpy(f_host).pin_memory()
         gp = torch.empty_like(fp).pin_memory()
         P.zeta(fp, out=gp)
@@ -340,33 +411,46 @@ def main():
         if world > 1:
             torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
         ems = float(ems.item())
-        e2e = {"value": world * units_step * args.e2e_steps / (ems / 1e3), "unit": "n·k·B gathers/s",
-               "h2d_bytes_per_step": 2 * n * B * 8, "d2h_bytes_per_step": 2 * n * B * 8,
-               "ms_per_step": ems / args.e2e_steps}
+        e2e = {"value": units_step * args.e2e_steps / (ems / 1e3), "unit": "n·k·B gathers/s",
+               "h2d_bytes_per_step": 2 * n * GB * 8, "d2h_bytes_per_step": 2 * n * GB * 8,
+               "ms_per_step": ems / args.e2e_steps,
+               "path": "poset_zeta + poset_moebius on pinned host buffers (library-staged copies)"}
         del fp, gp
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.chain import threads
         n_s = args.cpu_sample or min(wl.n, 1_000_000)
-        r = oracle_sample(wl, B, n_s, wl.dtype)
-        cpu = {"value": r["units"] / r["seconds"], "unit": "n·k·B gathers/s", "cores": 1,
-               "kind": "oracle",
-               "sample": (f"prefix n={n_s} of {args.config} (k={r['k']}, nnz={r['nnz']}), B={B} "
-                          f"{wl.dtype}, one zeta + one Möbius (Algs. 3-4), setup excluded, "
-                          f"{r['seconds']:.2f} s")}
+        O, fs = oracle_prefix(wl, B, n_s, wl.dtype)
+        t_par = oracle_time(O, fs, True)
+        t_seq = oracle_time(O, fs, False)
+        units = 2 * n_s * O.k * B
+        cpu = {"value": units / t_par, "unit": "n·k·B gathers/s", "cores": threads(),
+               "host_cores": host_cores(), "kind": "oracle",
+               "sample": (f"prefix n={n_s} of {args.config} (k={O.k}, nnz={O.nnz}), B={B} {wl.dtype}, "
+                          f"one zeta + one Möbius (Algs. 3-4; OpenMP, Möbius by Alg. 5), setup excluded, "
+                          f"{t_par:.2f} s"),
+               "single_core": {"value": units / t_seq, "cores": 1, "seconds": t_seq}}
+        del O, fs
 
+    prov = None
+    if rank == 0 and not args.no_provenance:
+        prov = {"sha256_edges": W.sha256_arrays(wl.src, wl.dst), "sha256_f_rank0": W.sha256_arrays(f_host),
+                "generator": "workloads.make_workload (numpy PCG64, DAG seed 0, values seed 1)"}
     if rank == 0:
         line = {
             "metric": "zeta/Möbius n·k gathers/s", "value": value, "unit": "n·k·B gathers/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
             "config": {"workload": args.config, "desc": wl.desc, "n": n, "k": k,
-                       "batch_per_rank": B, "global_batch": B * world, "ell": info["ell"],
+                       "batch_per_rank": B, "global_batch": GB, "ell": info["ell"],
                        "q": info["q"], "nnz": info["nnz"], "edges": info["m"],
                        "moebius_kernel": MOEB_NAMES[info["moebius_kernel"]],
                        "reach": info["reach"],
-                       "parallelism": f"column-shard x{world}",
+                       "parallelism": (f"zeta row-shard x{world} + NCCL all-gather, Möbius on rank 0"
+                                       if row_mode else f"column-shard x{world}"),
+                       "depth_u": P.info()["depth_u"], "provenance": prov,
                        "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
             "gbs_per_step": sum(ab[p] for p in kernels) / (ms_max / args.steps / 1e3) / 1e9,
             "roofline": roof, "zeta_roofline": zroof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
@@ -374,7 +458,8 @@ def main():
             "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
                       "match": info["t_match"], "chains": info["t_chains"],
                       "upload": info["t_upload"], "mtable": info["t_mtable"],
-                      "dist_table": info["t_dist"]},
+                      "dist_table": info["t_dist"], "gather_order_table_bytes": P.info()["gather_bytes"],
+                      "depth_u_seconds": P.info()["t_depth"]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -127,6 +127,11 @@ typedef struct {
     int64_t rdf_bytes;    /* bytes of the RINGDF / RINGCL near + far tables         */
     int64_t ring_bytes;   /* bytes of the RING tables (dist + next slot)            */
     int64_t rws_bytes;    /* bytes of the RINGWS tables                             */
+    int64_t depth_u;      /* D_U: longest dependency path of the U-solve (Alg. 4
+                             first loop), the PRAM depth bound of P:L740-745;
+                             -1 until poset_set_option("compute_depth_u", 1)   */
+    double t_depth;       /* seconds of that computation                            */
+    int64_t gather_bytes; /* bytes of the gather-order table (0 = not built yet)    */
 } poset_info;
 
 /*
@@ -220,8 +225,13 @@ poset_status poset_query(poset_t h, poset_info *out);
  * "ring_lpe" (lanes per element of the RING schedule, tuning);
  * "ringws_nwo" / "ringws_lpeo" (RINGWS warps / lanes per element, tuning);
  * "gather_variant" (process-wide dense zeta gather for batch % 32 == 0:
- * 0 = per-lane row reuse, 2 chains per step (default), 1 = lanes over
- * columns, 2 = lanes over ranks, 3 = per-lane row reuse, 4 chains per step);
+ * 0 = per-tile gather order with per-lane row reuse (default; its table,
+ * 4*n*k bytes, is built on the first such call), 1 = lanes over columns,
+ * 2 = lanes over ranks, 3 / 4 = rank-order per-lane row reuse with 4 / 2
+ * chains per step);
+ * "gather_pi_cfg" (process-wide, tuning: configuration of the gather-order
+ * kernel, 0 = default, 1..3 = alternatives measured in DESIGN.md §5.2);
+ * "compute_depth_u" (1: compute D_U now, synchronously, into poset_info.depth_u);
  * "profile" (0/1): record a CUDA event pair on the call's stream around every
  * kernel phase of subsequent calls (see poset_profile_read);
  * "ring_debug" (timing experiments only): bit 0 RING without the f store,

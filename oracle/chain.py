@@ -20,8 +20,14 @@ ERRORS = {-1: "cycle", -2: "self loop", -3: "invalid input", -4: "out of memory"
 
 
 def build(force: bool = False) -> str:
+    """gcc -O2; with -fopenmp for the parallel CPU baseline (oracle_*_omp)
+    when the compiler supports it, else single-threaded."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", _SRC, "-o", _SO])
+        base = ["gcc", "-O2", "-std=gnu99", "-shared", "-fPIC", _SRC, "-o", _SO]
+        try:
+            subprocess.check_call(base + ["-fopenmp"], stderr=subprocess.DEVNULL)
+        except subprocess.CalledProcessError:
+            subprocess.check_call(base)
     return _SO
 
 
@@ -37,7 +43,8 @@ def _load():
         lib.oracle_info.argtypes = [P, P]
         lib.oracle_export_chains.argtypes = [P, P, P, P, P]
         lib.oracle_export_niv.argtypes = [P, P]
-        for fn in (lib.oracle_zeta, lib.oracle_moebius):
+        lib.oracle_threads.restype = ctypes.c_int
+        for fn in (lib.oracle_zeta, lib.oracle_moebius, lib.oracle_zeta_omp, lib.oracle_moebius_omp):
             fn.argtypes = [P, P, P, i64, ctypes.c_int]
             fn.restype = ctypes.c_int
         lib.oracle_zeta_sampled.argtypes = [P, P, i64, ctypes.c_int, i64, P, P, P]
@@ -124,6 +131,23 @@ class ChainOracle:
             raise MemoryError("oracle_moebius")
         return f.reshape(g.shape)
 
+    def _run(self, fn, x):
+        x = np.ascontiguousarray(x)
+        x2 = x.reshape(self.n, -1)
+        y = np.empty_like(x2)
+        if fn(self._h, _ptr(x2), _ptr(y), x2.shape[1], self._dt(x2)):
+            raise MemoryError(fn.__name__)
+        return y.reshape(x.shape)
+
+    def zeta_omp(self, f):
+        """Alg. 3 with chains / rows in parallel (OpenMP, all threads)."""
+        return self._run(self._lib.oracle_zeta_omp, f)
+
+    def moebius_omp(self, g):
+        """Alg. 4 scheduled by Alg. 5 (antichains in order, elements of an
+        antichain in parallel, P:L692-705)."""
+        return self._run(self._lib.oracle_moebius_omp, g)
+
     def zeta_sampled(self, f, xs):
         """Brute-force g(x) = Σ_{y ⪯ x} f(y) for the user vertices ``xs`` only
         (DFS of ↓x); for fp64 also returns Σ_{y ⪯ x}|f(y)|."""
@@ -137,6 +161,11 @@ class ChainOracle:
         if rc:
             raise MemoryError("oracle_zeta_sampled")
         return g, ab
+
+
+def threads() -> int:
+    """OpenMP threads the parallel oracle uses (1 without OpenMP)."""
+    return int(_load().oracle_threads())
 
 
 def zeta_sampled_edges(n, src, dst, f, xs):

@@ -578,3 +578,150 @@ int oracle_zeta_sampled_edges(int64_t n, int64_t m, const int64_t *src, const in
     free(cp); free(ci); free(stk); free(seen);
     return 0;
 }
+
+/* ---------------- parallel CPU baseline (OpenMP) ---------------------------
+ * The same Algs. 3 and 4 scheduled as the paper's parallel CPU code: zeta
+ * with the chain prefix sums x' computed chain by chain (chains in parallel)
+ * and the rows y_i = sum_{j in niv(i)} x'_j in parallel ("for
+ * y = U x we can execute all dot products in parallel"); Moebius by Alg. 5
+ * (P:L692-705): the antichains L_1..L_ell of Alg. 6 in order, the elements of
+ * one antichain in parallel, a barrier between antichains; then the n - k
+ * subtractions y = y' - y'[next] in parallel (depth 1).  Every value
+ * is the same sum of the same terms as the sequential code, so int64 results
+ * are bit-identical (Z/2^64); fp64 sums each y_i in the same order too.
+ * Compiled with -fopenmp when available (oracle/chain.py); without it the
+ * loops run on one thread.  oracle_threads() reports the thread count. */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int oracle_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* chains bottom-up: order[cptr[c] .. cptr[c+1]) lists chain c from its lowest
+ * element (next[i] == i) to its top, paper indices */
+static int chain_lists(const oracle_poset *P, int32_t **order_out, int64_t **cptr_out, int32_t *kc_out) {
+    int32_t n = P->n;
+    char *pointed = calloc((size_t)n + 1, 1);
+    int32_t *order = malloc(sizeof(int32_t) * ((size_t)n + 1));
+    int64_t *cptr = malloc(sizeof(int64_t) * ((size_t)n + 2));
+    int32_t *stk = malloc(sizeof(int32_t) * ((size_t)n + 1));
+    if (!pointed || !order || !cptr || !stk) { free(pointed); free(order); free(cptr); free(stk); return -4; }
+    for (int32_t i = 1; i <= n; i++) if (P->next[i] != i) pointed[P->next[i]] = 1;
+    int32_t kc = 0;
+    int64_t w = 0;
+    for (int32_t top = 1; top <= n; top++) {
+        if (pointed[top]) continue;
+        int32_t len = 0, v = top;                 /* walk top -> bottom */
+        for (;;) { stk[len++] = v; if (P->next[v] == v) break; v = P->next[v]; }
+        cptr[kc++] = w;
+        while (len) order[w++] = stk[--len];      /* store bottom -> top */
+    }
+    cptr[kc] = w;
+    free(pointed); free(stk);
+    *order_out = order; *cptr_out = cptr; *kc_out = kc;
+    return 0;
+}
+
+#define OMP_ZETA(T)                                                                      \
+    do {                                                                                 \
+        const T *x = xin; T *y = yout;                                                   \
+        T *xp = calloc(((size_t)n + 1) * row, sizeof(T));                                \
+        if (!xp) { free(order); free(cptr); return -4; }                                 \
+        _Pragma("omp parallel for schedule(dynamic, 1)")                                 \
+        for (int32_t c = 0; c < kc; c++) {                                               \
+            for (int64_t t = cptr[c]; t < cptr[c + 1]; t++) {                            \
+                int32_t i = order[t];                                                    \
+                const T *xi = x + (size_t)P->user_of[i] * row;                           \
+                T *xpi = xp + (size_t)i * row;                                           \
+                if (t == cptr[c]) { for (size_t b = 0; b < row; b++) xpi[b] = xi[b]; }   \
+                else {                                                                   \
+                    const T *xpn = xp + (size_t)P->next[i] * row;                        \
+                    for (size_t b = 0; b < row; b++) xpi[b] = xpn[b] + xi[b];            \
+                }                                                                        \
+            }                                                                            \
+        }                                                                                \
+        _Pragma("omp parallel for schedule(static, 1024)")                               \
+        for (int32_t i = n; i >= 1; i--) {                                               \
+            T *yi = y + (size_t)P->user_of[i] * row;                                     \
+            for (size_t b = 0; b < row; b++) yi[b] = 0;                                  \
+            for (int64_t e = P->niv_ptr[i]; e < P->niv_ptr[i + 1]; e++) {                \
+                const T *xpj = xp + (size_t)P->niv[e] * row;                             \
+                for (size_t b = 0; b < row; b++) yi[b] += xpj[b];                        \
+            }                                                                            \
+        }                                                                                \
+        free(xp);                                                                        \
+    } while (0)
+
+int oracle_zeta_omp(const oracle_poset *P, const void *xin, void *yout, int64_t B, int dtype) {
+    int32_t n = P->n, kc = 0;
+    size_t row = (size_t)B;
+    int32_t *order = NULL;
+    int64_t *cptr = NULL;
+    if (chain_lists(P, &order, &cptr, &kc)) return -4;
+    if (dtype == 0) OMP_ZETA(uint64_t);
+    else OMP_ZETA(double);
+    free(order); free(cptr);
+    return 0;
+}
+
+#define OMP_MOEB(T)                                                                      \
+    do {                                                                                 \
+        const T *x = xin; T *y = yout;                                                   \
+        T *yp = calloc(((size_t)n + 1) * row, sizeof(T));                                \
+        if (!yp) { free(lv); free(lptr); return -4; }                                    \
+        _Pragma("omp parallel")                                                          \
+        for (int32_t L = 0; L < P->ell; L++) {          /* Alg. 5: antichain by antichain */ \
+            _Pragma("omp for schedule(static)")         /* implicit barrier = line 5 */  \
+            for (int64_t t = lptr[L]; t < lptr[L + 1]; t++) {                            \
+                int32_t i = lv[t];                                                       \
+                T *ypi = yp + (size_t)i * row;                                           \
+                const T *xi = x + (size_t)P->user_of[i] * row;                           \
+                for (size_t b = 0; b < row; b++) ypi[b] = xi[b];                         \
+                for (int64_t e = P->niv_ptr[i]; e < P->niv_ptr[i + 1]; e++) {            \
+                    int32_t j = P->niv[e];                                               \
+                    if (j == i) continue;                                                \
+                    const T *ypj = yp + (size_t)j * row;                                 \
+                    for (size_t b = 0; b < row; b++) ypi[b] -= ypj[b];                   \
+                }                                                                        \
+            }                                                                            \
+        }                                                                                \
+        _Pragma("omp parallel for schedule(static, 1024)")                               \
+        for (int32_t i = n; i >= 1; i--) {                                               \
+            T *yi = y + (size_t)P->user_of[i] * row;                                     \
+            const T *ypi = yp + (size_t)i * row;                                         \
+            if (P->next[i] != i) {                                                       \
+                const T *ypn = yp + (size_t)P->next[i] * row;                            \
+                for (size_t b = 0; b < row; b++) yi[b] = ypi[b] - ypn[b];                \
+            } else {                                                                     \
+                for (size_t b = 0; b < row; b++) yi[b] = ypi[b];                         \
+            }                                                                            \
+        }                                                                                \
+        free(yp);                                                                        \
+    } while (0)
+
+int oracle_moebius_omp(const oracle_poset *P, const void *xin, void *yout, int64_t B, int dtype) {
+    int32_t n = P->n;
+    size_t row = (size_t)B;
+    /* antichains of Alg. 6 as buckets: bucket L (0-based) = level L + 1
+     * (P->level is 1 for the leaves), elements of a bucket in ascending
+     * paper index */
+    int64_t *lptr = calloc((size_t)P->ell + 1, sizeof(int64_t));
+    int64_t *fill = calloc((size_t)P->ell + 1, sizeof(int64_t));
+    int32_t *lv = malloc(sizeof(int32_t) * ((size_t)n + 1));
+    if (!lptr || !fill || !lv) { free(lptr); free(fill); free(lv); return -4; }
+    for (int32_t i = 1; i <= n; i++) lptr[P->level[i]]++;
+    for (int32_t L = 0; L < P->ell; L++) lptr[L + 1] += lptr[L];
+    for (int32_t L = 0; L < P->ell; L++) fill[L] = lptr[L];
+    for (int32_t i = 1; i <= n; i++) lv[fill[P->level[i] - 1]++] = i;
+    free(fill);
+    if (dtype == 0) OMP_MOEB(uint64_t);
+    else OMP_MOEB(double);
+    free(lv); free(lptr);
+    return 0;
+}

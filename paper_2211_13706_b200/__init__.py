@@ -52,7 +52,8 @@ class PosetInfo(ctypes.Structure):
                 ("device", ctypes.c_int32), ("moebius_kernel", ctypes.c_int32),
                 ("reach", _i64), ("dist_bytes", _i64), ("t_dist", ctypes.c_double),
                 ("csr_bytes", _i64), ("zeta_sparse", _i64), ("ringws", _i64), ("ringdf", _i64),
-                ("rdf_bytes", _i64), ("ring_bytes", _i64), ("rws_bytes", _i64)]
+                ("rdf_bytes", _i64), ("ring_bytes", _i64), ("rws_bytes", _i64),
+                ("depth_u", _i64), ("t_depth", ctypes.c_double), ("gather_bytes", _i64)]
 
 
 def _sig(name, args, res=ctypes.c_int):

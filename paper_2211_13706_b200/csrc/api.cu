@@ -49,6 +49,8 @@ struct poset_s {
     RingDFPlan rdf;                   // RINGDF Möbius schedule (moebius_ringdf.cu)
     CsrRows csr;                      // sparse U-rows (moebius_csr.cu)
     bool zeta_csr = false;            // zeta gathers over the CSR rows (sparse table)
+    GatherPi gpi;                     // batched gather in the per-tile gather order (lazy)
+    bool gpi_failed = false;
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
     size_t gP_bytes = 0;
     // scratch, grown on demand
@@ -121,6 +123,7 @@ static void free_all(poset_s *h) {
     for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
     if (h->done_ev) cudaEventDestroy(h->done_ev);
+    free_gather_pi(h->gpi);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
                     h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
@@ -269,6 +272,7 @@ static poset_status finish_setup(poset_s *h) {
     I.rws_bytes = h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0;
     I.rdf_bytes = h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0;
     I.t_dist = t3 - t2;
+    I.depth_u = -1;
     I.csr_bytes = h->csr.ok ? h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8 : 0;
     I.zeta_sparse = h->zeta_csr ? 1 : 0;
     I.moebius_kernel = ringcl_fits(h->rdf) ? MOEB_RINGCL   // (for a batch that fits 2 SMs per column)
@@ -434,6 +438,23 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
         if (st) return st;
     }
     DevPoset P = h->dev();
+    // batched dense gather: build the gather-order table on first use (4nk
+    // bytes more; if it does not fit, the rank-order kernels stay in use)
+    const bool want_pi = !h->zeta_csr && B % 32 == 0 && gather_variant_get() == 0 && h->H.k > 0;
+    if (want_pi && !h->gpi.ok && !h->gpi_failed) {
+        size_t fb = 0, tb = 0;
+        CK(cudaMemGetInfo(&fb, &tb));
+        const size_t need = ((size_t)h->H.n + 256) * ((size_t)h->H.k + 2) * 4 + ((size_t)1 << 30);
+        cudaError_t e = need < fb ? build_gather_pi(P, h->gpi, s) : cudaErrorMemoryAllocation;
+        if (e != cudaSuccess) {
+            if (fatal_cuda_error(e)) CK(e);
+            cudaGetLastError();
+            free_gather_pi(h->gpi);
+            h->gpi_failed = true;
+        }
+    }
+    const bool use_pi = want_pi && h->gpi.ok;
+    h->info.gather_bytes = h->gpi.ok ? (int64_t)h->gpi.npad * (h->H.k + 1) * 4 + (h->gpi.npad / 256) * h->H.k * 8 : 0;
     {
         PhaseTimer t(h, POSET_PH_SCAN, s);
         CK(launch_scan(P, dt, f, h->d_F, 0, h->H.n, B, h->d_scan, nullptr, s));
@@ -442,6 +463,8 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
         PhaseTimer t(h, POSET_PH_GATHER, s);
         if (h->zeta_csr)
             CK(launch_gather_csr(P, h->csr, dt, h->d_F, g, 0, h->H.n, B, 0, s));
+        else if (use_pi)
+            CK(launch_gather_pi(h->gpi, h->H.k, dt, h->d_F, g, B, h->num_sms, s));
         else
             CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, h->num_sms, s));
     }
@@ -700,6 +723,7 @@ poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64
     I.q = H.q;
     I.ell = H.ell;
     I.nnz = -1;
+    I.depth_u = -1;
     I.table_bytes = (int64_t)H.n * H.k * 4;
     I.max_level_width = H.max_level_width;
     I.t_ingest = H.t_ingest;
@@ -767,8 +791,29 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)
-        if (value < 0 || value > 3) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0..3");
+        if (value < 0 || value > 4) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0..4");
         set_gather_variant((int)value);
+        return POSET_OK;
+    }
+    if (!strcmp(key, "gather_pi_cfg")) {   // process-wide gather-order kernel configuration (tuning)
+        if (value < 0 || value > 3) return fail(POSET_EINVAL, "poset_set_option: gather_pi_cfg is 0..3");
+        set_gather_pi_cfg((int)value);
+        return POSET_OK;
+    }
+    if (!strcmp(key, "compute_depth_u")) {
+        CK(cudaSetDevice(h->device));
+        double t0 = now_seconds();
+        int32_t *d_sr = nullptr, *d_D = nullptr;
+        cudaError_t e = upload(&d_sr, h->H.slot_rank);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d_D, std::max<size_t>((size_t)h->H.n * 4, 4));
+        if (e == cudaSuccess) e = launch_depth_u(h->dev(), d_sr, d_D, (unsigned *)h->d_count, 0);
+        unsigned du = 0;
+        if (e == cudaSuccess) e = cudaMemcpy(&du, h->d_count, sizeof du, cudaMemcpyDeviceToHost);
+        cudaFree(d_sr);
+        cudaFree(d_D);
+        CK(e);
+        h->info.depth_u = du;
+        h->info.t_depth = now_seconds() - t0;
         return POSET_OK;
     }
     if (!strcmp(key, "profile")) {

@@ -179,6 +179,46 @@ cudaError_t launch_count_nnz(const int32_t *M, int64_t total, int32_t n,
     return cudaGetLastError();
 }
 
+// ------------------------------------------- D_U: depth of the U-solve ----
+// D(r) = 1 + max { D(y) : y = chain_j[m(r,j)], j ≠ chain(r), m(r,j) ≥ 0 }
+// (1 with no cross-chain dependency); D_U = max_r D(r), the length of the
+// longest dependency path of Alg. 4's first loop -- the PRAM depth of the
+// triangular solve.  One CTA sweeps the levels in order (a
+// level's dependencies lie in lower levels); warp per element, lanes over
+// chains.  Diagnostic only (poset_set_option "compute_depth_u").
+__global__ void __launch_bounds__(1024) k_depth_u(DevPoset P, const int32_t *__restrict__ slot_rank,
+                                                  int32_t *D, unsigned *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned best = 0;
+    for (int32_t L = 0; L < P.ell; L++) {
+        const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        for (int32_t r = lo + warp; r < hi; r += 32) {
+            const int32_t c = P.chain[r];
+            int d = 0;
+            for (int32_t j = lane; j < P.k; j += 32) {
+                const int32_t sl = P.M[(size_t)j * P.n + r];
+                if (j != c && sl != P.n) d = max(d, D[slot_rank[sl]]);
+            }
+            d = __reduce_max_sync(0xffffffffu, d) + 1;
+            if (lane == 0) {
+                D[r] = d;
+                best = max(best, (unsigned)d);
+            }
+        }
+        __syncthreads();
+    }
+    if (lane == 0) atomicMax(out, best);
+}
+
+cudaError_t launch_depth_u(const DevPoset &P, const int32_t *slot_rank, int32_t *D, unsigned *out,
+                           cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess || P.n == 0) return e;
+    k_depth_u<<<1, 1024, 0, s>>>(P, slot_rank, D, out);
+    COUNT_LAUNCH(1);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------ (iii) segmented scan ----
 // Slot range [lo, lo+rows).  A CTA tile = RG row groups x CB columns; a
 // thread scans R consecutive slots of one column serially, row-group
@@ -696,11 +736,13 @@ __global__ void k_gather_reduce(const T *__restrict__ part, T *__restrict__ out,
 }
 
 // Dense-gather variant for B % 32 == 0 (process-wide; poset_set_option
-// "gather_variant"): 0 = k_gather_r4 (default), 1 = k_gather_cols,
-// 2 = k_gather (lanes over ranks).
+// "gather_variant"): 0 = gather order (gather_pi.cu; rank-order k_gather_r4
+// for row ranges and when the order table does not fit), 1 = k_gather_cols,
+// 2 = k_gather (lanes over ranks), 3 / 4 = k_gather_r4 with 4 / 2 chains per step.
 static std::atomic<int> g_gather_variant{0};
 void set_gather_variant(int v) { g_gather_variant = v; }
 static int gather_variant() { return g_gather_variant.load(); }
+int gather_variant_get() { return gather_variant(); }
 
 static int gather_cb(int64_t B) {
     for (int cb : {8, 4, 2, 1})
@@ -761,10 +803,10 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
                             int64_t B, int mode, void *partial, int num_sms, cudaStream_t s) {
     int S = gather_slices(P, hi - lo, B, num_sms);
     if (S > 1 && !partial) S = 1;
-    if (B % 32 == 0 && S == 1 && (gather_variant() == 0 || gather_variant() == 3)) {
+    if (B % 32 == 0 && S == 1 && (gather_variant() == 0 || gather_variant() == 3 || gather_variant() == 4)) {
         const int G32 = (int)(B / 32);
         const int64_t tiles = (hi - lo + 8 * 16 - 1) / (8 * 16);
-        if (gather_variant() == 0)   // 2 chains per step: fewer registers, 3 CTAs per SM (measured best)
+        if (gather_variant() != 3)   // 2 chains per step: fewer registers, 3 CTAs per SM (measured best)
             k_gather_r4<T, 64, 2, 3><<<(unsigned)(tiles * G32), 256, 0, s>>>(
                 P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         else

@@ -28,6 +28,10 @@ cudaError_t launch_mtable(const DevPoset &P, int32_t *M, cudaStream_t s);
 cudaError_t launch_count_nnz(const int32_t *M, int64_t total, int32_t n,
                              unsigned long long *out, cudaStream_t s);
 
+// ---- D_U, the dependency depth of the Möbius U-solve (diagnostic) ----
+cudaError_t launch_depth_u(const DevPoset &P, const int32_t *slot_rank, int32_t *D, unsigned *out,
+                           cudaStream_t s);
+
 // ---- kernel (iii): segmented chain scan F[slot] = prefix of f[user(slot)] ----
 // Scans slots [slot_lo, slot_hi).  carry-in of the first rows is 0 (the
 // split-phase API adds remote carries with launch_scan_carry).  tail (nullable):
@@ -52,6 +56,23 @@ size_t gather_partial_bytes(const DevPoset &P, int64_t rows, int64_t batch, int 
 cudaError_t launch_gather(const DevPoset &P, int dtype, const void *F, void *g, int64_t row_lo,
                           int64_t row_hi, int64_t batch, int out_rank, void *partial,
                           int num_sms, cudaStream_t s);
+
+// ---- kernel (iv), batched form (gather_pi.cu): B % 32 == 0, the index table
+// re-laid in a per-tile greedy gather order (built lazily on the first such
+// call) ----
+struct GatherPi {
+    bool ok = false;
+    int64_t npad = 0;            // n rounded up to the 256-element tile
+    int32_t *Mg = nullptr;       // [k][npad] F slots in gather order (n = ∞ / padding)
+    int32_t *out_user = nullptr; // [npad] user id of each position (-1 = padding)
+    void *Fr = nullptr;          // [npad/256][k] int2 F-slot range per (tile, chain) (L2 prefetch)
+};
+cudaError_t build_gather_pi(const DevPoset &P, GatherPi &G, cudaStream_t s);
+void free_gather_pi(GatherPi &G);
+cudaError_t launch_gather_pi(const GatherPi &G, int32_t k, int dtype, const void *F, void *g, int64_t B,
+                             int num_sms, cudaStream_t s);
+int gather_variant_get();
+void set_gather_pi_cfg(int c);   // tuning: kernel configuration of the gather-order kernel
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
 enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5,

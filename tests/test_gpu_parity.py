@@ -302,7 +302,7 @@ def test_ragged_batches_and_1d():
     assert (host(P.zeta(dev(f1))) == O.zeta(f1)).all()
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_dense_gather_variants(variant):
     """The three dense zeta-gather kernels for batch % 32 == 0 agree with O2
     (bit-exact int64, tolerance fp64), including a ragged rank tail."""

@@ -368,3 +368,16 @@ def test_zeta_sampled_edges_is_pinned_to_O1(case):
     gf, ab = zeta_sampled_edges(n, src, dst, ff, xs)
     assert_fp64_close(gf, brute.zeta(n, src, dst, ff)[xs], brute.zeta_abs(n, src, dst, ff)[xs])
     np.testing.assert_allclose(ab, brute.zeta_abs(n, src, dst, ff)[xs], rtol=1e-12)
+
+
+@pytest.mark.parametrize("case", list(_edge_sample_cases()), ids=lambda c: c[0])
+def test_parallel_oracle_equals_sequential(case):
+    """The OpenMP CPU baseline (chains / rows in parallel; Möbius by Alg. 5,
+    antichain by antichain) sums the same terms in the same
+    order as the sequential Algs. 3-4: identical bits for int64 and fp64."""
+    name, n, src, dst = case
+    O = ChainOracle(n, src, dst)
+    for f in (W.int_values(n, 5, -10**18, 10**18, seed=2), W.normal_values(n, 3, seed=3)):
+        g = O.zeta(f)
+        assert np.array_equal(O.zeta_omp(f), g)
+        assert np.array_equal(O.moebius_omp(g), O.moebius(g))
