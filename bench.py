@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--moebius-kernel", default="auto", choices=MOEB_NAMES)
     ap.add_argument("--gather-variant", type=int, default=0, help="dense gather kernel for B%%32==0 (tuning)")
     ap.add_argument("--gather-pi-cfg", type=int, default=0, help="gather-order kernel configuration (tuning)")
+    ap.add_argument("--ringcl-helpers", type=int, default=0, help="RINGCL helper CTAs (tuning; 0 = auto)")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -272,6 +273,8 @@ def main():
     P.set_option("gather_pi_cfg", args.gather_pi_cfg)
     if args.ring_debug:
         P.set_option("ring_debug", args.ring_debug)
+    if args.ringcl_helpers:
+        P.set_option("ringcl_helpers", args.ringcl_helpers)
     # strong scaling (default): BASELINE's global batch split over the ranks
     # by columns (no data-path collective); a single function (batch < world)
     # is row-sharded for zeta (NCCL all-gathers, dist.row_sharded_zeta) with
@@ -330,6 +333,8 @@ def main():
     ms = e0.elapsed_time(e1)
     prof, launches = P.profile_read()
     P.set_option("profile", 0)
+    if args.ring_debug:
+        print("ring_debug counters:", P.debug_read().tolist(), file=sys.stderr, flush=True)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
