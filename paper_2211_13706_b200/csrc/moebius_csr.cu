@@ -15,10 +15,10 @@
 //                  are summed by 32 lanes in parallel instead of one thread:
 //                    F(x) = g(x) - Σ_{s ∈ U-row(x)} F[s];  f(x) = F(x) - F(next(x))
 //
-// Two lane mappings: lanes over the row's entries (B < 32, one column at a
-// time, warp-shuffle reduction) or lanes over columns (B % 32 == 0; each row
-// entry is read once by the warp and broadcast by a shuffle, the F row is one
-// coalesced 256-B load).
+// Two lane mappings: lanes over the row's entries (B % 32 != 0, one column
+// at a time, warp-shuffle reduction) or lanes over columns (B % 32 == 0; each
+// row entry is read once by the warp and broadcast by a shuffle, the F row is
+// one coalesced 256-B load).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -109,11 +109,10 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + c] by one warp, lanes over entries; the
 // result is valid in every lane.  CG: loads bypass L1 (data written earlier
 // in the same kernel by other SMs).  8 independent loads per lane in flight.
-template <typename T, bool CG>
+template <typename T, bool CG, int U = 16>
 __device__ __forceinline__ T row_sum_lanes(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                            const T *Fsrc, int32_t B, int c) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = 16;
     T s[U];
 #pragma unroll
     for (int u = 0; u < U; u++) s[u] = T(0);
@@ -142,11 +141,10 @@ __device__ __forceinline__ T row_sum_lanes(const int32_t *__restrict__ idx, int6
 // Σ_{e ∈ [a, b)} Fsrc[idx[e] * B + col] by one warp, lanes over columns: the
 // row entries are read 32 at a time and broadcast by shuffles; 16 row loads
 // (one coalesced 256-B load each) in flight.
-template <typename T, bool CG>
+template <typename T, bool CG, int U = 32>
 __device__ __forceinline__ T row_sum_cols(const int32_t *__restrict__ idx, int64_t a, int64_t b,
                                           const T *Fsrc, int32_t B, int col) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = 32;
     T s[U];
 #pragma unroll
     for (int u = 0; u < U; u++) s[u] = T(0);
@@ -244,39 +242,82 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks, unsig
     __syncthreads();
 }
 
+// One level's items (element, 32-column group) are dealt to "item slots":
+// groups of WPI warps inside a CTA (1024 threads = 32 / WPI slots per CTA).
+// The WPI warps of a slot split the element's row into contiguous chunks,
+// sum them (lanes over columns, or over entries for B < 32), reduce their
+// partial sums through shared memory under the slot's named barrier, and the
+// slot's first warp writes F(x) = g(x) - Σ and f(x) = F(x) - F(next(x)).
+// A level of w elements uses ceil(w * G / slots) rounds; C4w (256 x 2
+// items) and C3w (~360 items) fit one round on 148 CTAs x 4 slots, so each
+// level costs one L2 round trip of row loads, a shared-memory reduction and
+// the grid barrier (the round-1 kernel used one warp per item, so a level of
+// C4w ran 512 warps of 255 serial-ish loads each on a 4,736-warp grid).
+constexpr int kCsrWPI = 8;                    // warps per item slot
+constexpr int kCsrSlots = 32 / kCsrWPI;       // item slots per 1024-thread CTA
+
 template <typename T, bool COLS>
-__global__ void __launch_bounds__(512) k_moeb_csr(DevPoset P, const int64_t *__restrict__ ptr,
-                                                  const int32_t *__restrict__ idx,
-                                                  const T *__restrict__ g, T *F, T *__restrict__ f,
-                                                  int32_t B, int G, unsigned *bar) {
-    const int64_t TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t *__restrict__ ptr,
+                                                      const int32_t *__restrict__ idx,
+                                                      const T *__restrict__ g, T *F, T *__restrict__ f,
+                                                      int32_t B, int G, unsigned *bar) {
+    __shared__ T part[kCsrSlots][kCsrWPI][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = warp / kCsrWPI, ws = warp % kCsrWPI;
+    const int64_t nslots = (int64_t)gridDim.x * kCsrSlots;
+    const int64_t my_slot = (int64_t)blockIdx.x * kCsrSlots + slot;
     for (int32_t L = 0; L < P.ell; L++) {
         const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
         const int64_t items = (int64_t)(hi - lo) * G;
-        for (int64_t it = gw; it < items; it += TW) {
-            const int32_t r = lo + (int32_t)(it / G);
-            const int cg = (int)(it % G);
-            const int64_t a = ptr[r], b = ptr[r + 1];
-            const int32_t my = P.slot[r], u = P.rank_user[r];
-            const bool has_prev = !(P.slot_user[my] < 0);   // bit 31 = chain start
+        // every slot runs the same number of rounds (named barriers inside)
+        const int64_t rounds = (items + nslots - 1) / nslots;
+        for (int64_t rd = 0; rd < rounds; rd++) {
+            const int64_t it = my_slot + rd * nslots;
+            const bool valid = it < items;
+            int32_t r = 0, my = 0, u = 0;
+            int cg = 0;
+            int64_t a = 0, b = 0;
+            if (valid) {
+                r = lo + (int32_t)(it / G);
+                cg = (int)(it % G);
+                a = ptr[r];
+                b = ptr[r + 1];
+            }
+            // this warp's chunk of the row
+            const int64_t len = b - a, per = (len + kCsrWPI - 1) / kCsrWPI;
+            const int64_t ca = a + min(len, per * ws), cb = a + min(len, per * (ws + 1));
             if (COLS) {
                 const int col = cg * 32 + lane;
-                const T s = row_sum_cols<T, true>(idx, a, b, F, B, col);
-                const T Fx = __ldg(g + (size_t)u * B + col) - s;
-                F[(size_t)my * B + col] = Fx;
-                f[(size_t)u * B + col] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + col) : Fx;
+                const T s = valid ? row_sum_cols<T, true, 8>(idx, ca, cb, F, B, col) : T(0);
+                part[slot][ws][lane] = s;
             } else {
-                for (int c = 0; c < B; c++) {
-                    const T s = row_sum_lanes<T, true>(idx, a, b, F, B, c);
-                    if (lane == 0) {
-                        const T Fx = __ldg(g + (size_t)u * B + c) - s;
-                        F[(size_t)my * B + c] = Fx;
-                        f[(size_t)u * B + c] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + c) : Fx;
-                    }
+                // B % 32 != 0: lanes over entries, one column of the group at
+                // a time; lane c of the partial row holds column cg * 32 + c
+                T mine = T(0);
+                const int c1 = min(B - cg * 32, 32);
+                for (int c = 0; c < c1; c++) {
+                    const T s = valid ? row_sum_lanes<T, true, 8>(idx, ca, cb, F, B, cg * 32 + c) : T(0);
+                    if (lane == c) mine = s;
+                }
+                part[slot][ws][lane] = mine;
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
+            if (ws == 0 && valid) {
+                my = P.slot[r];
+                u = P.rank_user[r];
+                const bool has_prev = !(P.slot_user[my] < 0);   // bit 31 = chain start
+                const int ncol = COLS ? 32 : min(B - cg * 32, 32);
+                if (lane < ncol) {
+                    const int col = cg * 32 + lane;
+                    T s = part[slot][0][lane];
+#pragma unroll
+                    for (int w2 = 1; w2 < kCsrWPI; w2++) s += part[slot][w2][lane];
+                    const T Fx = __ldg(g + (size_t)u * B + col) - s;
+                    F[(size_t)my * B + col] = Fx;
+                    f[(size_t)u * B + col] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + col) : Fx;
                 }
             }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
         }
         if (L + 1 < P.ell) grid_sync(bar, gridDim.x, (unsigned)L);
     }
@@ -286,18 +327,16 @@ cudaError_t launch_moebius_csr(const DevPoset &P, const CsrRows &C, int dtype, c
                                void *F, void *f, int64_t B, unsigned *bar, int num_sms,
                                cudaStream_t s) {
     if (P.n == 0) return cudaSuccess;
+    // lanes over columns for B % 32 == 0; otherwise lanes over entries, one
+    // column at a time, in groups of 32 columns
     const bool cols = B % 32 == 0;
-    int G = cols ? (int)(B / 32) : 1;
+    int G = (int)((B + 31) / 32);
     void *fn;
     if (dtype == 0)
         fn = cols ? (void *)k_moeb_csr<u64, true> : (void *)k_moeb_csr<u64, false>;
     else
         fn = cols ? (void *)k_moeb_csr<double, true> : (void *)k_moeb_csr<double, false>;
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, 0);
-    if (e != cudaSuccess) return e;
-    per_sm = std::max(1, std::min(per_sm, 2));
-    e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
+    cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     DevPoset Pc = P;
     const int64_t *pp = C.ptr;
@@ -305,7 +344,7 @@ cudaError_t launch_moebius_csr(const DevPoset &P, const CsrRows &C, int dtype, c
     int32_t Bi = (int32_t)B;
     void *args[] = {&Pc, &pp, &ip, (void *)&g, &F, &f, &Bi, &G, &bar};
     launches_add(1);
-    return cudaLaunchCooperativeKernel(fn, dim3(num_sms * per_sm), dim3(512), args, 0, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(num_sms), dim3(1024), args, 0, s);
 }
 
 }  // namespace poset
