@@ -70,7 +70,7 @@ typedef enum {
     POSET_ECYCLE = 3,         /* the edges contain a directed cycle (S:L48 CycleError)           */
     POSET_ENOTCHAIN = 4,      /* injected chain with consecutive incomparable elements  */
     POSET_ENOTPARTITION = 5,  /* injected chains do not partition 0..n-1                */
-    POSET_ETOOBIG = 6,        /* dense n*k*4-byte table + buffers exceed free device memory      */
+    POSET_ETOOBIG = 6,        /* neither the dense n*k*4-byte table nor the sparse rows fit      */
     POSET_ENOMEM = 7,         /* host allocation, or a device scratch allocation, failed (not sticky) */
     POSET_ECUDA = 8           /* CUDA error (no device, launch failure, ...) -- sticky           */
 } poset_status;
@@ -145,6 +145,23 @@ typedef struct {
  */
 poset_status poset_setup(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
                          int device, poset_t *out);
+
+/* poset_setup_ex flags */
+enum {
+    POSET_SETUP_SPARSE = 1    /* never build the dense table: the U-rows (the paper's sparse N,
+                                 P:L292) are built straight from the DAG, level by level (Thm. 4,
+                                 P:L356-367), and zeta / Möbius run over them.
+                                 poset_setup does this on its own when the dense n*k table does
+                                 not fit in device memory.                                  */
+};
+
+/*
+ * poset_setup_ex -- poset_setup with flags (POSET_SETUP_SPARSE).  Errors as
+ * poset_setup; EINVAL for unknown flags; ETOOBIG only when neither the dense
+ * table nor the sparse rows fit.
+ */
+poset_status poset_setup_ex(int64_t n, int64_t m, const int64_t *src, const int64_t *dst, int device,
+                            uint32_t flags, poset_t *out);
 
 /*
  * poset_setup_chains -- as poset_setup, but with an injected chain

@@ -64,6 +64,7 @@ def _sig(name, args, res=ctypes.c_int):
 
 
 _sig("poset_setup", [_i64, _i64, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)])
+_sig("poset_setup_ex", [_i64, _i64, _vp, _vp, ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(_vp)])
 _sig("poset_setup_chains", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)])
 _sig("poset_zeta", [_vp, _vp, _vp, _i64, ctypes.c_int, _vp])
 _sig("poset_moebius", [_vp, _vp, _vp, _i64, ctypes.c_int, _vp])
@@ -161,17 +162,20 @@ class Poset:
 
     ``src``/``dst``: int64 edge arrays, edge e meaning ``dst[e] ⪯ src[e]``.
     ``chains``: optional injected chain decomposition (list of user-id lists,
-    each top-down) -- ``poset_setup_chains``.
+    each top-down) -- ``poset_setup_chains``.  ``sparse``: build only the
+    sparse rows, straight from the DAG (``POSET_SETUP_SPARSE``); the library
+    also does this on its own when the dense table does not fit.
     """
 
-    def __init__(self, n: int, src, dst, device: int = 0, chains=None):
+    def __init__(self, n: int, src, dst, device: int = 0, chains=None, sparse: bool = False):
         src = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
         dst = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
         if src.shape != dst.shape:
             raise ValueError("src and dst must have the same length")
         h = _vp()
         if chains is None:
-            rc = lib.poset_setup(n, src.shape[0], _np_ptr(src), _np_ptr(dst), device, ctypes.byref(h))
+            rc = lib.poset_setup_ex(n, src.shape[0], _np_ptr(src), _np_ptr(dst), device, 1 if sparse else 0,
+                                    ctypes.byref(h))
         else:
             ptr = np.zeros(len(chains) + 1, dtype=np.int64)
             ptr[1:] = np.cumsum([len(c) for c in chains])

@@ -49,6 +49,8 @@ struct poset_s {
     RingDFPlan rdf;                   // RINGDF Möbius schedule (moebius_ringdf.cu)
     CsrRows csr;                      // sparse U-rows (moebius_csr.cu)
     bool zeta_csr = false;            // zeta gathers over the CSR rows (sparse table)
+    bool sparse_only = false;         // no dense table M: rows built straight from the DAG (N1)
+    unsigned setup_flags = 0;
     GatherPi gpi;                     // batched gather in the per-tile gather order (lazy)
     bool gpi_failed = false;
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
@@ -141,6 +143,77 @@ static cudaError_t upload(T **dst, const std::vector<T> &v) {
     return e;
 }
 
+// Sparse mode: the dense table does not fit (or the
+// caller asked for POSET_SETUP_SPARSE) -- the U-rows are built straight from
+// the DAG (build_csr_direct) and every transform runs over them: zeta by
+// k_gather_csr, Möbius by the CSR schedule.  The schedules that need the
+// dense table (ring family, LEVEL / GRID / WARP, the gather order) are off.
+static poset_status finish_setup_sparse(poset_s *h, double t0, size_t table, size_t free_b) {
+    HostPoset &H = h->H;
+    CK(upload(&h->d_rank_user, H.rank_user));
+    CK(upload(&h->d_slot, H.slot));
+    CK(upload(&h->d_chain, H.chain));
+    CK(upload(&h->d_lvl, H.lvl_ptr));
+    CK(upload(&h->d_child_ptr, H.child_ptr));
+    CK(upload(&h->d_child, H.child));
+    CK(upload(&h->d_slot_user, H.slot_user));
+    CK(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
+    CK(cudaMalloc((void **)&h->d_bar, 64));
+    CK(cudaMalloc((void **)&h->d_count, 64));
+    int32_t *d_slot_chain = nullptr, *d_chain_off = nullptr;
+    {
+        std::vector<int32_t> sc((size_t)H.n);
+        for (int32_t sl = 0; sl < H.n; sl++) sc[sl] = H.chain[H.slot_rank[sl]];
+        CK(upload(&d_slot_chain, sc));
+        CK(upload(&d_chain_off, H.chain_off));
+    }
+    CK(cudaDeviceSynchronize());
+    double t1 = now_seconds();
+    size_t fb = 0, tb = 0;
+    CK(cudaMemGetInfo(&fb, &tb));
+    // room left for F / g / f / staging of a batch: max(2 GiB, 1/8 of free)
+    const size_t reserve = std::max<size_t>((size_t)2 << 30, fb / 8);
+    DevPoset P = h->dev();
+    cudaError_t e = build_csr_direct(P, H.lvl_ptr.data(), d_slot_chain, d_chain_off, h->csr,
+                                     fb > reserve ? fb - reserve : 0, H.max_level_width, 0);
+    cudaFree(d_slot_chain);
+    cudaFree(d_chain_off);
+    CK(e);
+    if (!h->csr.ok) {
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "poset_setup: neither the dense table (%.2f GB, n=%d, k=%d) nor the sparse rows fit "
+                 "(%.2f GB free)", table / 1e9, H.n, H.k, free_b / 1e9);
+        return fail(POSET_ETOOBIG, buf);
+    }
+    h->sparse_only = true;
+    h->zeta_csr = true;
+    double t2 = now_seconds();
+    poset_info &I = h->info;
+    I.n = H.n;
+    I.m = H.m;
+    I.k = H.k;
+    I.q = H.q;
+    I.ell = H.ell;
+    I.nnz = h->csr.nnz + H.n;   // + the self entries
+    I.table_bytes = (int64_t)table;
+    I.max_level_width = H.max_level_width;
+    I.t_ingest = H.t_ingest;
+    I.t_levels = H.t_levels;
+    I.t_match = H.t_match;
+    I.t_chains = H.t_chains;
+    I.t_upload = t1 - t0;
+    I.t_mtable = t2 - t1;   // the sparse rows take the dense table's place
+    I.device = h->device;
+    I.csr_bytes = h->csr.nnz * 4 + ((int64_t)H.n + 1) * 8;
+    I.zeta_sparse = 1;
+    I.moebius_kernel = MOEB_CSR;
+    I.depth_u = -1;
+    std::vector<int32_t>().swap(H.child);
+    std::vector<int64_t>().swap(H.child_ptr);
+    return POSET_OK;
+}
+
 static poset_status finish_setup(poset_s *h) {
     HostPoset &H = h->H;
     double t0 = now_seconds();
@@ -153,13 +226,8 @@ static poset_status finish_setup(poset_s *h) {
     CK(cudaMemGetInfo(&free_b, &total_b));
     h->info.table_bytes = (int64_t)table;
     h->info.k = H.k;
-    if (resident + (size_t)(H.n + 1) * 8 * 4 > free_b) {
-        char buf[256];
-        snprintf(buf, sizeof buf,
-                 "poset_setup: dense table needs %.2f GB (n=%d, k=%d) but %.2f GB are free",
-                 table / 1e9, H.n, H.k, free_b / 1e9);
-        return fail(POSET_ETOOBIG, buf);
-    }
+    const bool dense_fits = resident + (size_t)(H.n + 1) * 8 * 4 <= free_b;
+    if (!dense_fits || (h->setup_flags & POSET_SETUP_SPARSE)) return finish_setup_sparse(h, t0, table, free_b);
     CK(upload(&h->d_rank_user, H.rank_user));
     CK(upload(&h->d_slot, H.slot));
     CK(upload(&h->d_chain, H.chain));
@@ -289,7 +357,7 @@ static poset_status finish_setup(poset_s *h) {
 
 static poset_status setup_common(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
                                  int64_t k, const int64_t *cp, const int64_t *ce, bool inject,
-                                 int device, poset_t *out) {
+                                 int device, poset_t *out, unsigned flags = 0) {
     if (!out) return fail(POSET_EINVAL, "poset_setup: out is null");
     *out = nullptr;
     int ndev = 0;
@@ -300,6 +368,7 @@ static poset_status setup_common(int64_t n, int64_t m, const int64_t *src, const
     poset_s *h = new (std::nothrow) poset_s();
     if (!h) return fail(POSET_ENOMEM, "poset_setup: out of host memory");
     h->device = device;
+    h->setup_flags = flags;
     std::string err;
     poset_status st;
     try {
@@ -325,6 +394,12 @@ static poset_status setup_common(int64_t n, int64_t m, const int64_t *src, const
 }
 
 extern "C" {
+
+poset_status poset_setup_ex(int64_t n, int64_t m, const int64_t *src, const int64_t *dst, int device,
+                            uint32_t flags, poset_t *out) {
+    if (flags & ~(uint32_t)POSET_SETUP_SPARSE) return fail(POSET_EINVAL, "poset_setup_ex: unknown flags");
+    return setup_common(n, m, src, dst, 0, nullptr, nullptr, false, device, out, flags);
+}
 
 poset_status poset_setup(int64_t n, int64_t m, const int64_t *src, const int64_t *dst, int device,
                          poset_t *out) {
@@ -483,6 +558,9 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
                 : h->ring.ok ? MOEB_RING
                 : h->csr.ok  ? MOEB_CSR
                              : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+    if (h->sparse_only && which != MOEB_CSR)
+        return fail(POSET_EINVAL, "poset_moebius: sparse-rows poset (no dense table): only the CSR schedule "
+                                  "applies; use AUTO");
     if (which == MOEB_CSR) {
         if (!h->csr.ok)
             return fail(POSET_EINVAL, "poset_moebius: the CSR schedule has no sparse rows for this "
@@ -801,6 +879,7 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "compute_depth_u")) {
+        if (h->sparse_only) return fail(POSET_EINVAL, "compute_depth_u: needs the dense table (sparse-rows poset)");
         CK(cudaSetDevice(h->device));
         double t0 = now_seconds();
         int32_t *d_sr = nullptr, *d_D = nullptr;
@@ -872,6 +951,23 @@ poset_status poset_debug_read(poset_t h, int64_t *out8) {
 poset_status poset_export_mtable(poset_t h, int32_t *out) {
     if (!h || !out) return fail(POSET_EINVAL, "poset_export_mtable: null argument");
     const HostPoset &H = h->H;
+    if (h->sparse_only) {   // from the U-rows: own chain = pos(x), the rest from the row, ∞ = -1
+        std::vector<int64_t> ptr((size_t)H.n + 1);
+        std::vector<int32_t> idx((size_t)std::max<int64_t>(h->csr.nnz, 1));
+        CK(cudaSetDevice(h->device));
+        CK(cudaMemcpy(ptr.data(), h->csr.ptr, ptr.size() * 8, cudaMemcpyDeviceToHost));
+        if (h->csr.nnz) CK(cudaMemcpy(idx.data(), h->csr.idx, (size_t)h->csr.nnz * 4, cudaMemcpyDeviceToHost));
+        for (int32_t r = 0; r < H.n; r++) {
+            int32_t *row = out + (size_t)H.rank_user[r] * H.k;
+            for (int32_t j = 0; j < H.k; j++) row[j] = -1;
+            row[H.chain[r]] = H.pos[r];
+            for (int64_t e = ptr[r]; e < ptr[r + 1]; e++) {
+                const int32_t sl = idx[e], q = H.slot_rank[sl];
+                row[H.chain[q]] = H.pos[q];
+            }
+        }
+        return POSET_OK;
+    }
     std::vector<int32_t> M((size_t)H.n * H.k);
     CK(cudaSetDevice(h->device));
     if (!M.empty()) CK(cudaMemcpy(M.data(), h->d_M, M.size() * 4, cudaMemcpyDeviceToHost));

@@ -189,6 +189,13 @@ struct CsrRows {
 // Builds the rows from the dense table if they fit in free_budget bytes
 // (C.ok = false otherwise; not an error).
 cudaError_t build_csr(const DevPoset &P, CsrRows &C, size_t free_budget);
+// The same rows straight from the DAG, level by level, without M (N1):
+// budget = device bytes the rows may take; C.ok = false if they do not fit.
+// slot_chain[s] = chain of slot s; chain_off[k+1] = chain starts (device);
+// h_lvl_ptr = host level bounds.
+cudaError_t build_csr_direct(const DevPoset &P, const int32_t *h_lvl_ptr, const int32_t *slot_chain,
+                             const int32_t *chain_off, CsrRows &C, size_t budget, int32_t max_level_width,
+                             cudaStream_t s);
 cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *F,
                               void *g, int64_t row_lo, int64_t row_hi, int64_t batch,
                               int out_rank, cudaStream_t s);

@@ -92,6 +92,218 @@ cudaError_t build_csr(const DevPoset &P, CsrRows &C, size_t free_budget) {
     return cudaSuccess;
 }
 
+// ------------------------------------------------ build without M (N1) ---
+// The U-rows straight from the DAG, level by level, without the dense n x k
+// table (the paper's sparse N, built bottom-up as in
+// Alg. 2): by Thm. 4 the full niv row of x is the
+// per-chain maximum over its children c of (U-row(c) ∪ {slot(c)}) -- slots
+// are sorted by chain, then position, so "per-chain maximum" is "the last
+// entry of each chain run" of the merged, sorted slot lists.  Entries on x's
+// own chain are dropped (its own entry is implicit: slot(x)).
+// One warp per element: lane i owns the chains [i k / 32, (i+1) k / 32), i.e.
+// a contiguous slot range (chains are laid out contiguously), finds its
+// segment of every child's row by binary search and merges it (m-way merge,
+// m = out-degree <= 64); lane counts -> a warp prefix sum -> the element's
+// row.  A count pass, a prefix sum over the level and a fill pass per level.
+constexpr int kDirectMaxChildren = 64;
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t lo, int64_t hi, int32_t v) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_csr_direct(int32_t lo, int32_t hi, int32_t k,
+                                                    const int64_t *__restrict__ child_ptr,
+                                                    const int32_t *__restrict__ child,
+                                                    const int32_t *__restrict__ slot,
+                                                    const int32_t *__restrict__ chain,
+                                                    const int32_t *__restrict__ slot_chain,
+                                                    const int32_t *__restrict__ chain_off, int64_t *ptr,
+                                                    int32_t *idx, int64_t *cnt, int32_t *too_many) {
+    const int lane = threadIdx.x & 31;
+    const int32_t r = lo + (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= hi) return;
+    const int64_t c0 = child_ptr[r], c1 = child_ptr[r + 1];
+    const int m = (int)(c1 - c0);
+    if (m > kDirectMaxChildren) {
+        if (lane == 0) *too_many = 1;
+        return;
+    }
+    // this lane's slot range
+    const int32_t s_lo = chain_off[(int64_t)lane * k / 32], s_hi = chain_off[(int64_t)(lane + 1) * k / 32];
+    const int32_t own_lo = chain_off[chain[r]], own_hi = chain_off[chain[r] + 1];
+    int64_t cur[kDirectMaxChildren], end[kDirectMaxChildren];
+    int32_t cs[kDirectMaxChildren];   // slot(c) if in this lane's range and not yet taken, else INT32_MAX
+    for (int i = 0; i < m; i++) {
+        const int32_t c = child[c0 + i];
+        const int64_t a = ptr[c], b = ptr[c + 1];
+        cur[i] = s_lo > 0 ? lower_bound_i32(idx, a, b, s_lo) : a;
+        end[i] = lower_bound_i32(idx, cur[i], b, s_hi);
+        const int32_t sc = slot[c];
+        cs[i] = (sc >= s_lo && sc < s_hi) ? sc : INT32_MAX;
+    }
+    int64_t w = 0;
+    int32_t prev = -1, prev_chain = -1;
+    int64_t o = 0;
+    if (FILL) {
+        // this lane's output offset: the lane counts of the count pass are
+        // recomputed here (cheaper than storing 32 counts per element)
+    }
+    // pass 1 (always): count; pass 2 (FILL): write at the lane's offset
+    for (int pass = 0; pass < (FILL ? 2 : 1); pass++) {
+        if (pass == 1) {
+            // exclusive prefix of the lane counts
+            int64_t x = w;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            o = ptr[r] + x - w;
+            // rewind the cursors
+            for (int i = 0; i < m; i++) {
+                const int32_t c = child[c0 + i];
+                const int64_t a = ptr[c], b = ptr[c + 1];
+                cur[i] = s_lo > 0 ? lower_bound_i32(idx, a, b, s_lo) : a;
+                const int32_t sc = slot[c];
+                cs[i] = (sc >= s_lo && sc < s_hi) ? sc : INT32_MAX;
+            }
+            w = 0;
+            prev = -1;
+            prev_chain = -1;
+        }
+        for (;;) {
+            int32_t best = INT32_MAX;
+            int bi = -1;
+            bool from_row = false;
+            for (int i = 0; i < m; i++) {
+                const int32_t hr = cur[i] < end[i] ? idx[cur[i]] : INT32_MAX;
+                if (hr < best) { best = hr; bi = i; from_row = true; }
+                if (cs[i] < best) { best = cs[i]; bi = i; from_row = false; }
+            }
+            if (bi < 0) break;
+            if (from_row) cur[bi]++;
+            else cs[bi] = INT32_MAX;
+            if (best == prev) continue;                       // the same slot from several children
+            if (best >= own_lo && best < own_hi) continue;    // own chain: implicit
+            const int32_t ch = slot_chain[best];
+            if (ch == prev_chain) {
+                if (pass == 1) idx[o + w - 1] = best;   // a higher slot of the same chain: the max wins
+            } else {
+                if (pass == 1) idx[o + w] = best;
+                w++;
+            }
+            prev = best;
+            prev_chain = ch;
+        }
+    }
+    if (!FILL) {
+        int64_t t = w;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+        if (lane == 0) cnt[r - lo] = t;
+    }
+}
+
+// ptr[lo + i] = base + Σ_{t < i} cnt[t], ptr[hi] = base + Σ cnt (one CTA)
+__global__ void __launch_bounds__(1024) k_csr_direct_scan(int32_t lo, int32_t hi, const int64_t *cnt,
+                                                          int64_t *ptr) {
+    __shared__ int64_t sh[1024];
+    const int t = threadIdx.x;
+    const int32_t w = hi - lo;
+    const int32_t per = (w + 1023) / 1024;
+    const int32_t a = min(w, t * per), b = min(w, a + per);
+    int64_t s = 0;
+    for (int32_t i = a; i < b; i++) s += cnt[i];
+    sh[t] = s;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+        const int64_t v = t >= d ? sh[t - d] : 0;
+        __syncthreads();
+        sh[t] += v;
+        __syncthreads();
+    }
+    const int64_t base = ptr[lo];
+    __syncthreads();
+    int64_t run = base + (t ? sh[t - 1] : 0);
+    for (int32_t i = a; i < b; i++) {
+        ptr[lo + i] = run;
+        run += cnt[i];
+    }
+    if (t == 1023) ptr[hi] = base + sh[1023];
+}
+
+cudaError_t build_csr_direct(const DevPoset &P, const int32_t *h_lvl_ptr, const int32_t *slot_chain,
+                             const int32_t *chain_off, CsrRows &C, size_t budget, int32_t max_level_width,
+                             cudaStream_t s) {
+    C.ok = false;
+    const int32_t n = P.n;
+    if (n == 0) return cudaSuccess;
+    const size_t ptr_bytes = ((size_t)n + 1) * 8;
+    if (budget < ptr_bytes + 4096) return cudaSuccess;
+    const size_t cap = (budget - ptr_bytes) / 4;   // idx entries that fit
+    cudaError_t e = cudaMalloc((void **)&C.ptr, ptr_bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); C.ptr = nullptr; return cudaSuccess; }
+    e = cudaMalloc((void **)&C.idx, cap * 4);
+    if (e != cudaSuccess) { cudaGetLastError(); cudaFree(C.ptr); C.ptr = nullptr; C.idx = nullptr; return cudaSuccess; }
+    int64_t *cnt = nullptr, *h_total = nullptr;
+    int32_t *flag = nullptr;
+    e = cudaMalloc((void **)&cnt, (size_t)std::max(max_level_width, 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&flag, 4);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&h_total, 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(C.ptr, 0, 8, s);
+    bool full = false;
+    int64_t total = 0;
+    for (int32_t L = 0; L < P.ell && e == cudaSuccess; L++) {
+        const int32_t lo = h_lvl_ptr[L], hi = h_lvl_ptr[L + 1];
+        const unsigned blocks = (unsigned)(((int64_t)(hi - lo) * 32 + 127) / 128);
+        k_csr_direct<false><<<blocks, 128, 0, s>>>(lo, hi, P.k, P.child_ptr, P.child, P.slot, P.chain, slot_chain,
+                                                   chain_off, C.ptr, C.idx, cnt, flag);
+        k_csr_direct_scan<<<1, 1024, 0, s>>>(lo, hi, cnt, C.ptr);
+        // the level's rows must fit the allocation before they are written
+        e = cudaMemcpyAsync(h_total, C.ptr + hi, 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) break;
+        const int64_t level_rows = *h_total - total;
+        total = *h_total;
+        // stop as soon as the rows cannot fit: this level's, or the rest at
+        // this level's average row length (rows grow with the level on the
+        // generators, so this only under-estimates)
+        if ((size_t)total > cap ||
+            (double)total + (double)(n - hi) * ((double)level_rows / (hi - lo)) > (double)cap) {
+            full = true;
+            break;
+        }
+        k_csr_direct<true><<<blocks, 128, 0, s>>>(lo, hi, P.k, P.child_ptr, P.child, P.slot, P.chain, slot_chain,
+                                                  chain_off, C.ptr, C.idx, cnt, flag);
+        launches_add(3);
+        e = cudaGetLastError();
+    }
+    int32_t too_many = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&too_many, flag, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(cnt);
+    cudaFree(flag);
+    if (h_total) cudaFreeHost(h_total);
+    if (e != cudaSuccess) return e;
+    if (full || too_many) {   // does not fit / unsupported: no rows
+        cudaFree(C.ptr);
+        cudaFree(C.idx);
+        C.ptr = nullptr;
+        C.idx = nullptr;
+        return cudaSuccess;
+    }
+    C.nnz = total;
+    C.ok = true;
+    return cudaSuccess;
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_cg(const T *p);
 template <>
