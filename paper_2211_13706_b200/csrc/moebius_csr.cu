@@ -416,10 +416,57 @@ __global__ void __launch_bounds__(256) k_gather_csr(DevPoset P, const int64_t *_
     }
 }
 
+// Short rows (the paper's ER DAGs: ~10-80 entries) and B < 32: one thread
+// per (rank, column), the row's loads unrolled 8-wide (a warp per row would
+// leave most lanes idle).
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather_csr_thread(DevPoset P, const int64_t *__restrict__ ptr,
+                                                           const int32_t *__restrict__ idx,
+                                                           const T *__restrict__ F, T *__restrict__ out,
+                                                           int64_t row_lo, int64_t row_hi, int32_t B,
+                                                           int mode) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = row_lo + t / B;
+    const int c = (int)(t % B);
+    if (r >= row_hi) return;
+    const int64_t a = ptr[r], b = ptr[r + 1];
+    constexpr int U = 8;
+    T acc[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) acc[u] = T(0);
+    int64_t e = a;
+    for (; e + U <= b; e += U) {
+        int32_t i[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) i[u] = __ldg(idx + e + u);
+#pragma unroll
+        for (int u = 0; u < U; u++) acc[u] += __ldg(F + (size_t)i[u] * B + c);
+    }
+    for (; e < b; e++) acc[0] += __ldg(F + (size_t)__ldg(idx + e) * B + c);
+#pragma unroll
+    for (int st = 1; st < U; st <<= 1)
+#pragma unroll
+        for (int u = 0; u < U; u += 2 * st) acc[u] += acc[u + st];
+    T *dst = mode == 0 ? out + (size_t)P.rank_user[r] * B : out + (size_t)(r - row_lo) * B;
+    dst[c] = acc[0] + __ldg(F + (size_t)P.slot[r] * B + c);
+}
+
 cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, const void *F,
                               void *g, int64_t lo, int64_t hi, int64_t B, int out_rank,
                               cudaStream_t s) {
     if (hi <= lo) return cudaSuccess;
+    if (B % 32 != 0 && (double)C.nnz / P.n < 96) {
+        const int64_t threads = (hi - lo) * B;
+        const unsigned blocks = (unsigned)((threads + 255) / 256);
+        launches_add(1);
+        if (dtype == 0)
+            k_gather_csr_thread<u64><<<blocks, 256, 0, s>>>(P, C.ptr, C.idx, (const u64 *)F, (u64 *)g, lo, hi,
+                                                            (int32_t)B, out_rank);
+        else
+            k_gather_csr_thread<double><<<blocks, 256, 0, s>>>(P, C.ptr, C.idx, (const double *)F, (double *)g, lo,
+                                                               hi, (int32_t)B, out_rank);
+        return cudaGetLastError();
+    }
     const bool cols = B % 32 == 0;
     const int G = cols ? (int)(B / 32) : 1;
     const int64_t warps = (hi - lo) * G;
@@ -465,14 +512,15 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks, unsig
 // level costs one L2 round trip of row loads, a shared-memory reduction and
 // the grid barrier (the round-1 kernel used one warp per item, so a level of
 // C4w ran 512 warps of 255 serial-ish loads each on a 4,736-warp grid).
-constexpr int kCsrWPI = 8;                    // warps per item slot
-constexpr int kCsrSlots = 32 / kCsrWPI;       // item slots per 1024-thread CTA
-
-template <typename T, bool COLS>
+// WPI (warps per item slot) follows the average row length: 8 for the
+// long rows of C2 / C3w / C4w, 4 for medium rows, 1 (a warp per element, no
+// slot barrier) for the short rows of the paper's ER DAGs.
+template <typename T, bool COLS, int kCsrWPI>
 __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t *__restrict__ ptr,
                                                       const int32_t *__restrict__ idx,
                                                       const T *__restrict__ g, T *F, T *__restrict__ f,
                                                       int32_t B, int G, unsigned *bar) {
+    constexpr int kCsrSlots = 32 / kCsrWPI;   // item slots per 1024-thread CTA
     __shared__ T part[kCsrSlots][kCsrWPI][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = warp / kCsrWPI, ws = warp % kCsrWPI;
@@ -513,7 +561,8 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t 
                 }
                 part[slot][ws][lane] = mine;
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
+            if (kCsrWPI > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
+            else __syncwarp();
             if (ws == 0 && valid) {
                 my = P.slot[r];
                 u = P.rank_user[r];
@@ -529,7 +578,51 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t 
                     f[(size_t)u * B + col] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + col) : Fx;
                 }
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
+            if (kCsrWPI > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
+            else __syncwarp();
+        }
+        if (L + 1 < P.ell) grid_sync(bar, gridDim.x, (unsigned)L);
+    }
+}
+
+// Short rows (ER DAGs, ~10-80 entries) and B < 32: one thread per
+// (element, column) sums its row (8 loads in flight), persistent grid with
+// one barrier per level as above.
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) k_moeb_csr_thread(DevPoset P, const int64_t *__restrict__ ptr,
+                                                             const int32_t *__restrict__ idx,
+                                                             const T *__restrict__ g, T *F, T *__restrict__ f,
+                                                             int32_t B, unsigned *bar) {
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int32_t L = 0; L < P.ell; L++) {
+        const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        const int64_t items = (int64_t)(hi - lo) * B;
+        for (int64_t it = tid; it < items; it += nth) {
+            const int32_t r = lo + (int32_t)(it / B);
+            const int c = (int)(it % B);
+            const int64_t a = ptr[r], b = ptr[r + 1];
+            constexpr int U = 8;
+            T acc[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) acc[u] = T(0);
+            int64_t e = a;
+            for (; e + U <= b; e += U) {
+                int32_t i[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) i[u] = __ldg(idx + e + u);
+#pragma unroll
+                for (int u = 0; u < U; u++) acc[u] += ld_cg(F + (size_t)i[u] * B + c);
+            }
+            for (; e < b; e++) acc[0] += ld_cg(F + (size_t)__ldg(idx + e) * B + c);
+#pragma unroll
+            for (int st = 1; st < U; st <<= 1)
+#pragma unroll
+                for (int u = 0; u < U; u += 2 * st) acc[u] += acc[u + st];
+            const int32_t my = P.slot[r], usr = P.rank_user[r];
+            const T Fx = __ldg(g + (size_t)usr * B + c) - acc[0];
+            F[(size_t)my * B + c] = Fx;
+            f[(size_t)usr * B + c] = P.slot_user[my] < 0 ? Fx : Fx - ld_cg(F + (size_t)(my - 1) * B + c);
         }
         if (L + 1 < P.ell) grid_sync(bar, gridDim.x, (unsigned)L);
     }
@@ -539,15 +632,34 @@ cudaError_t launch_moebius_csr(const DevPoset &P, const CsrRows &C, int dtype, c
                                void *F, void *f, int64_t B, unsigned *bar, int num_sms,
                                cudaStream_t s) {
     if (P.n == 0) return cudaSuccess;
+    if (B % 32 != 0 && (double)C.nnz / P.n < 128) {
+        cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
+        if (e != cudaSuccess) return e;
+        DevPoset Pc = P;
+        const int64_t *pp = C.ptr;
+        const int32_t *ip = C.idx;
+        int32_t Bi = (int32_t)B;
+        void *args[] = {&Pc, &pp, &ip, (void *)&g, &F, &f, &Bi, &bar};
+        void *fn = dtype == 0 ? (void *)k_moeb_csr_thread<u64> : (void *)k_moeb_csr_thread<double>;
+        launches_add(1);
+        return cudaLaunchCooperativeKernel(fn, dim3(num_sms), dim3(1024), args, 0, s);
+    }
     // lanes over columns for B % 32 == 0; otherwise lanes over entries, one
     // column at a time, in groups of 32 columns
     const bool cols = B % 32 == 0;
     int G = (int)((B + 31) / 32);
+    const double avg = (double)C.nnz / P.n;
+    const int wpi = avg >= 128 ? 8 : avg >= 48 ? 4 : 1;
     void *fn;
-    if (dtype == 0)
-        fn = cols ? (void *)k_moeb_csr<u64, true> : (void *)k_moeb_csr<u64, false>;
-    else
-        fn = cols ? (void *)k_moeb_csr<double, true> : (void *)k_moeb_csr<double, false>;
+#define MCSR(WPI)                                                                                  \
+    if (wpi == WPI) {                                                                              \
+        if (dtype == 0)                                                                            \
+            fn = cols ? (void *)k_moeb_csr<u64, true, WPI> : (void *)k_moeb_csr<u64, false, WPI>;  \
+        else                                                                                       \
+            fn = cols ? (void *)k_moeb_csr<double, true, WPI> : (void *)k_moeb_csr<double, false, WPI>; \
+    }
+    MCSR(1) MCSR(4) MCSR(8)
+#undef MCSR
     cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     DevPoset Pc = P;

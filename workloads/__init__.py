@@ -260,6 +260,13 @@ def _lay(forced):
     return b
 
 
+def _er(n0, delta):
+    def b(scale):
+        n = max(2, int(n0 * scale))
+        return (n,) + erdos_renyi(n, delta, 0)
+    return b
+
+
 CONFIGS = {
     "C1": (_c1, 1, "i64", (-100, 100), "random DAG n=1000, min(i,3) edges into [i-50,i)"),
     "C2": (_c2, 1, "f64", None, "Boolean lattice 2^16"),
@@ -269,6 +276,13 @@ CONFIGS = {
     "C4w": (_lay(True), 64, "i64", (-1000, 1000), "layered 4096x256 width-bounded"),
     "C5": (_win(16_000_000, 64, False), 32, "f64", None, "window DAG n=16M W=64 (literal)"),
     "C5w": (_win(16_000_000, 64, True), 32, "f64", None, "window DAG n=16M W=64 width-bounded"),
+    # literal C4 through the sparse rows (N1): one function (B=64 would be
+    # 64 x the gathers of a 3.1e10-entry table)
+    "C4lit1": (_lay(False), 1, "i64", (-1000, 1000), "layered 4096x256 (literal, sparse rows), B=1"),
+    # the paper's own workload (§5): Erdos-Renyi DAGs,
+    # average degree 4 and 6, n = 9M (its largest size); one fp64 function
+    "ER4": (_er(9_000_000, 4), 1, "f64", None, "Erdos-Renyi DAG n=9M, delta=4 (paper §5)"),
+    "ER6": (_er(9_000_000, 6), 1, "f64", None, "Erdos-Renyi DAG n=9M, delta=6 (paper §5)"),
 }
 
 
