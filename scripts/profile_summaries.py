@@ -1,13 +1,16 @@
 """Write the committed ncu summaries under profiles/ from a gpurun_out capture:
-  python scripts/profile_summaries.py <tag> <launches.csv> <full.ncu-rep> <bench-cmd>
--> profiles/r1_launches_C5w.csv, r1_launches_C5w_summary.md, r1_ncu_full_C5w.md,
-   ncu_traffic.json (DRAM bytes per launch of the step kernels)."""
+  python scripts/profile_summaries.py <round> <launches.csv> <full.ncu-rep | raw.csv> <bench-cmd>
+-> profiles/<round>_launches_C5w.csv, <round>_launches_C5w_summary.md,
+   <round>_ncu_full_C5w.md, ncu_traffic.json (DRAM bytes per launch of the
+   step kernels).  The third argument may be the report's raw page as CSV
+   (`ncu -i rep --page raw --csv`), written on the GPU box when the report
+   is too large to copy back."""
 import csv, collections, json, os, re, shutil, subprocess, sys
 
 tag, launches, rep, cmd = sys.argv[1:5]
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 prof = os.path.join(root, "profiles")
-shutil.copy(launches, os.path.join(prof, "r1_launches_C5w.csv"))
+shutil.copy(launches, os.path.join(prof, f"{tag}_launches_C5w.csv"))
 
 # launch list: kernel name, duration
 rows = [r for r in csv.reader(open(launches)) if len(r) > 5]
@@ -42,7 +45,7 @@ out += ["", "Step kernels only (share of the step; compare with bench.py's `kern
 for k, v in sorted(step.items(), key=lambda x: -x[1][1]):
     per = v[1] / v[0] * scale
     out.append(f"| `{k}` | {per:.3f} | {per / step_ms:.3f} |")
-open(os.path.join(prof, "r1_launches_C5w_summary.md"), "w").write("\n".join(out) + "\n")
+open(os.path.join(prof, f"{tag}_launches_C5w_summary.md"), "w").write("\n".join(out) + "\n")
 
 # full capture
 metrics = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -52,13 +55,15 @@ metrics = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
            "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
            "launch__cluster_dim_x", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = (open(rep).read() if rep.endswith(".csv")
+       else subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rr = list(csv.reader(raw.splitlines()))
 h, units = rr[0], rr[1]
 out = [f"# ncu --set full, C5w full size (n=16M, B=32 fp64), first launch of each step kernel", "",
-       f"`ncu --set full --clock-control none --import-source on -k regex:\"k_moeb_ringcl|k_gather_r4|k_scan_tiles|k_to_rank_major\" -c 5` on `{cmd}`.", ""]
+       f"`ncu --set full --clock-control none --import-source on` (kernels: the step's) on `{cmd}`.", ""]
 traffic = {}
-keymap = {"k_scan_tiles": "scan", "k_gather_r4": "gather", "k_to_rank_major": "perm", "k_moeb_ringcl": "moebius_solve"}
+keymap = {"k_scan_tiles": "scan", "k_scan_carry_tiles": "scan", "k_gather_r4": "gather", "k_gather_pi": "gather",
+          "k_to_rank_major": "perm", "k_moeb_ringcl": "moebius_solve"}
 for row in rr[2:]:
     kn = row[h.index("Kernel Name")]
     out.append(f"## {kn}")
@@ -67,13 +72,15 @@ for row in rr[2:]:
             out.append(f"- {m} = {row[h.index(m)]} {units[h.index(m)]}")
     out.append("")
     for pre, key in keymap.items():
-        if pre in kn:
+        if re.search(r"\b" + pre + r"\b", kn):
             def gb(m):
                 v = float(row[h.index(m)].replace(",", ""))
                 u = units[h.index(m)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             traffic[key] = traffic.get(key, 0.0) + gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
-open(os.path.join(prof, "r1_ncu_full_C5w.md"), "w").write("\n".join(out) + "\n")
-json.dump({"C5w": traffic, "_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from profiles/r1_ncu_full_C5w.md (scan = both scan-tile passes)"},
+open(os.path.join(prof, f"{tag}_ncu_full_C5w.md"), "w").write("\n".join(out) + "\n")
+ent = {k: {"bytes": v, "capture": f"profiles/{tag}_ncu_full_C5w.md"} for k, v in traffic.items()}
+json.dump({"C5w": ent, "_note": f"dram__bytes_read.sum + dram__bytes_write.sum per launch from profiles/{tag}_ncu_full_C5w.md "
+           "(scan = both scan-tile passes + the carry pass)"},
           open(os.path.join(prof, "ncu_traffic.json"), "w"), indent=1)
 print(json.dumps(traffic))
