@@ -461,6 +461,9 @@ def main():
                        "depth_u": P.info()["depth_u"], "provenance": prov,
                        "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
             "gbs_per_step": sum(ab[p] for p in kernels) / (ms_max / args.steps / 1e3) / 1e9,
+            # nnz(N)·B per second: the work the method needs;
+            # n·k·B above counts the dense table's entries, ∞ included
+            "value_nnz": 2 * info["nnz"] * GB * args.steps / (ms_max / 1e3),
             "roofline": roof, "zeta_roofline": zroof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "round_trip_exact": ok,
             "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
