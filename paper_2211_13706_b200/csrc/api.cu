@@ -505,7 +505,7 @@ typedef poset_status (*device_fn)(poset_s *, const void *, void *, int64_t, int,
 static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int dt, cudaStream_t s) {
     poset_status st = ensure_F(h, B, s);
     if (st) return st;
-    st = grow(h, &h->d_scan, &h->scan_bytes, scan_scratch_bytes(h->H.n, B));
+    st = grow(h, &h->d_scan, &h->scan_bytes, std::max(scan_scratch_bytes(h->H.n, B), scan1p_scratch_bytes(h->H.n, B)));
     if (st) return st;
     size_t pb = gather_partial_bytes(h->dev(), h->H.n, B, h->num_sms);
     if (pb) {
@@ -532,7 +532,10 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
     h->info.gather_bytes = h->gpi.ok ? (int64_t)h->gpi.npad * (h->H.k + 1) * 4 + (h->gpi.npad / 256) * h->H.k * 8 : 0;
     {
         PhaseTimer t(h, POSET_PH_SCAN, s);
-        CK(launch_scan(P, dt, f, h->d_F, 0, h->H.n, B, h->d_scan, nullptr, s));
+        if (B <= 4)   // single pass (decoupled look-back); measured slower than the three-kernel scan for B = 32, 64
+            CK(launch_scan_1p(P, dt, f, h->d_F, B, h->d_scan, s));
+        else
+            CK(launch_scan(P, dt, f, h->d_F, 0, h->H.n, B, h->d_scan, nullptr, s));
     }
     {
         PhaseTimer t(h, POSET_PH_GATHER, s);

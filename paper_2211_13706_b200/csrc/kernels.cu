@@ -384,6 +384,146 @@ cudaError_t launch_scan(const DevPoset &P, int dtype, const void *f, void *F, in
                       : scan_t<double>(P, f, F, lo, hi, B, scratch, tail, s);
 }
 
+// ---------------------------------------- (iii) single-pass scan (zeta) ----
+// Decoupled look-back: one pass over f.  Tiles of RG row groups x CB columns
+// (R = 16 slots per thread, kept in registers) are taken in slot order from
+// an atomic ticket (so every predecessor is running or done); a tile
+// publishes its aggregate (flag, value) per column, looks back over its
+// predecessors' published aggregates / inclusive prefixes until it meets a
+// prefix or a chain start (the segmented operator restarts there), publishes
+// its own inclusive prefix, and writes F from the registers.  f is read once
+// and F written once: 16nB bytes (the three-kernel scan above read f twice).
+// status[(t * B + b)]: {value, flag | state << 1}, state 0 = empty,
+// 1 = aggregate, 2 = inclusive prefix.
+struct ScanStatus { unsigned long long v; unsigned long long fs; };
+
+template <typename T>
+__device__ __forceinline__ void st_status(ScanStatus *p, T v, unsigned fl, unsigned state) {
+    const unsigned long long bits = to_bits<T>(v);
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(bits),
+                 "l"((unsigned long long)(fl | (state << 1)))
+                 : "memory");
+}
+template <typename T>
+__device__ __forceinline__ unsigned ld_status(const ScanStatus *p, T &v, unsigned &fl) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    v = from_bits<T>(a);
+    fl = (unsigned)(b & 1u);
+    return (unsigned)(b >> 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_scan_1p(const T *__restrict__ f, T *__restrict__ F,
+                                                 const int32_t *__restrict__ slot_user, int64_t rows,
+                                                 int32_t B, int CB, int RG, ScanStatus *status,
+                                                 unsigned *ticket, int64_t ntiles) {
+    constexpr int R = 16;
+    __shared__ T sv[256];
+    __shared__ int sf[256];
+    __shared__ T sexcl[32];
+    __shared__ int sexf[32];
+    __shared__ int64_t stile;
+    const int bl = threadIdx.x % CB, rg = threadIdx.x / CB;
+    const int b = blockIdx.y * CB + bl;
+    const bool act = rg < RG && b < B;
+    if (threadIdx.x == 0) stile = atomicAdd(ticket + blockIdx.y, 1u);
+    __syncthreads();
+    const int64_t t = stile;
+    const int64_t s0 = t * (int64_t)RG * R + (int64_t)rg * R;
+    T x[R];
+    int st[R];
+    T v = T(0);
+    int fl = 0;
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        const int64_t sl = s0 + i;
+        x[i] = T(0);
+        st[i] = 0;
+        if (act && sl < rows) {
+            const int32_t u = slot_user[sl];
+            st[i] = u < 0;
+            x[i] = f[(size_t)(u & 0x7fffffff) * B + b];
+            if (st[i]) { fl = 1; v = T(0); }
+            v += x[i];
+        }
+    }
+    seg_block_scan<T>(v, fl, rg, bl, RG, CB, sv, sf);
+    // tile aggregate per column = inclusive value of the last row group
+    if (act && rg == RG - 1) {
+        ScanStatus *my = status + (size_t)t * B + b;
+        if (t == 0) {
+            st_status<T>(my, v, (unsigned)fl, 2u);
+            sexcl[bl] = T(0);
+            sexf[bl] = 0;
+        } else {
+            st_status<T>(my, v, (unsigned)fl, 1u);
+            // look back: running = (predecessors' aggregates) ⊕ ..., right to left
+            T run = T(0);
+            int rf = 0;
+            for (int64_t p = t - 1;; p--) {
+                T pv;
+                unsigned pf, state;
+                do { state = ld_status<T>(status + (size_t)p * B + b, pv, pf); } while (state == 0);
+                run = rf ? run : pv + run;   // (pf, pv) ⊕ (rf, run)
+                rf |= (int)pf;
+                if (state == 2 || pf) break;
+            }
+            sexcl[bl] = run;
+            sexf[bl] = rf;
+            // this tile's inclusive prefix = exclusive ⊕ aggregate
+            const T inc = fl ? v : run + v;
+            st_status<T>(my, inc, (unsigned)(fl | rf), 2u);
+        }
+    }
+    __syncthreads();
+    if (!act) return;
+    // this row group's exclusive prefix: tile exclusive ⊕ earlier row groups
+    T run = sexcl[bl];
+    if (rg > 0) {
+        const T pv = sv[(rg - 1) * CB + bl];
+        const int pf = sf[(rg - 1) * CB + bl];
+        run = pf ? pv : run + pv;
+    }
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        const int64_t sl = s0 + i;
+        if (sl < rows) {
+            if (st[i]) run = T(0);
+            run += x[i];
+            F[(size_t)sl * B + b] = run;
+        }
+    }
+}
+
+size_t scan1p_scratch_bytes(int64_t rows, int64_t B) {
+    ScanGeom g = scan_geom(rows, B);
+    return (size_t)std::max<int64_t>(g.ntiles, 1) * B * sizeof(ScanStatus) + 64 * sizeof(unsigned) + 256;
+}
+
+template <typename T>
+static cudaError_t scan1p_t(const DevPoset &P, const void *f, void *F, int64_t B, void *scratch,
+                            cudaStream_t s) {
+    const int64_t rows = P.n;
+    if (rows <= 0) return cudaSuccess;
+    ScanGeom g = scan_geom(rows, B);
+    if (g.gy > 64) return cudaErrorInvalidValue;   // B > 2048: the caller uses the three-kernel scan
+    ScanStatus *status = reinterpret_cast<ScanStatus *>(scratch);
+    unsigned *ticket = reinterpret_cast<unsigned *>(status + (size_t)g.ntiles * B);
+    cudaError_t e = cudaMemsetAsync(scratch, 0, scan1p_scratch_bytes(rows, B), s);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)g.ntiles, (unsigned)g.gy);
+    k_scan_1p<T><<<grid, 256, 0, s>>>((const T *)f, (T *)F, P.slot_user, rows, (int32_t)B, g.CB, g.RG, status,
+                                      ticket, g.ntiles);
+    COUNT_LAUNCH(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_1p(const DevPoset &P, int dtype, const void *f, void *F, int64_t B, void *scratch,
+                           cudaStream_t s) {
+    return dtype == 0 ? scan1p_t<u64>(P, f, F, B, scratch, s) : scan1p_t<double>(P, f, F, B, scratch, s);
+}
+
 template <typename T>
 __global__ void k_add_carry(T *F, const T *carry, int64_t lo, int64_t end, int32_t B) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

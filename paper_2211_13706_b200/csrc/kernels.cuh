@@ -41,6 +41,11 @@ size_t scan_scratch_bytes(int64_t rows, int64_t batch);
 cudaError_t launch_scan(const DevPoset &P, int dtype, const void *f, void *F, int64_t slot_lo,
                         int64_t slot_hi, int64_t batch, void *scratch, void *tail,
                         cudaStream_t s);
+// The whole slot range in one pass (decoupled look-back, f read once): the
+// zeta transform's scan.  scratch: scan1p_scratch_bytes(n, batch) bytes.
+size_t scan1p_scratch_bytes(int64_t rows, int64_t batch);
+cudaError_t launch_scan_1p(const DevPoset &P, int dtype, const void *f, void *F, int64_t batch, void *scratch,
+                           cudaStream_t s);
 cudaError_t launch_scan_carry(const DevPoset &P, int dtype, void *F, const void *carry,
                               int64_t slot_lo, int64_t slot_hi, int64_t batch, cudaStream_t s);
 
