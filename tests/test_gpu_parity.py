@@ -323,6 +323,25 @@ def test_dense_gather_variants(variant):
         P.set_option("gather_variant", 0)
 
 
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_gather_order_configs(cfg):
+    """The gather-order kernel's configurations (option gather_pi_cfg)
+    against O2, bit-exact int64 and fp64 within the tolerance, with ∞
+    entries (the bottom of the poset) and a ragged tile."""
+    n = 7003
+    src, dst = W.window_dag(n, 2, 64, 9, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    P.set_option("gather_pi_cfg", cfg)
+    try:
+        for B in (32, 64):
+            f = W.int_values(n, B, -10**15, 10**15, seed=B + cfg)
+            assert (gpu_zeta(P, f) == O.zeta(f)).all(), B
+            ff = W.normal_values(n, B, seed=B + 2)
+            assert_fp64_close(gpu_zeta(P, ff), O.zeta(ff), O.zeta(np.abs(ff)))
+    finally:
+        P.set_option("gather_pi_cfg", 0)
+
+
 def test_host_buffers_and_inplace():
     n = 5000
     src, dst = W.window_dag(n, 2, 64, 5, forced=True)
