@@ -242,7 +242,13 @@ static poset_status finish_setup(poset_s *h) {
     CK(cudaDeviceSynchronize());
     double t1 = now_seconds();
     DevPoset P = h->dev();
-    CK(launch_mtable(P, h->d_M, 0));
+    {
+        int64_t creach = 0;   // rank distance of the farthest child (host CSR, rank space)
+        for (int32_t r = 0; r < H.n; r++)
+            for (int64_t t = H.child_ptr[r]; t < H.child_ptr[r + 1]; t++)
+                creach = std::max<int64_t>(creach, r - H.child[t]);
+        CK(launch_mtable(P, h->d_M, 0, (int32_t)std::min<int64_t>(creach, INT32_MAX / 2), H.max_level_width));
+    }
     CK(launch_count_nnz(h->d_M, (int64_t)H.n * H.k, H.n, h->d_count, 0));
     unsigned long long nnz = 0;
     CK(cudaMemcpy(&nnz, h->d_count, sizeof nnz, cudaMemcpyDeviceToHost));

@@ -149,8 +149,89 @@ __global__ void __launch_bounds__(128) k_mtable(DevPoset P, int32_t *M) {
     }
 }
 
-cudaError_t launch_mtable(const DevPoset &P, int32_t *M, cudaStream_t s) {
+// The same propagation with chain j's recent values in a shared-memory ring
+// (rank mod RING, RING >= the children's rank reach + the widest level) and
+// the next level's child lists, chain ids and slots prefetched into
+// registers one level ahead: the per-level chain of a warp is then ring
+// loads -> max -> ring store -> __syncwarp instead of dependent global
+// loads (~1 µs per level on C5w, 630k levels).  One warp (CTA) per chain.
+constexpr int kMtCh = 4;   // children prefetched per element (more: loaded in place)
+__global__ void __launch_bounds__(32) k_mtable_ring(DevPoset P, int32_t *M, int ring_mask) {
+    extern __shared__ int32_t mring[];
+    const int lane = threadIdx.x;
+    const int j = blockIdx.x;
+    const int32_t n = P.n;
+    int32_t *Mj = M + (size_t)j * n;
+    // prefetched first pass of the next level: element, chain, slot, children
+    int32_t nr = -1, nchain = -1, nslot = 0, nc[kMtCh], nhi = 0;
+    int64_t na = 0, nb = 0;
+    auto fetch = [&](int32_t L) {
+        nr = -1;
+        if (L >= P.ell) return;
+        const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        nhi = hi;
+        const int32_t r = lo + lane;
+        if (r < hi) {
+            nr = r;
+            nchain = P.chain[r];
+            nslot = P.slot[r];
+            na = P.child_ptr[r];
+            nb = P.child_ptr[r + 1];
+#pragma unroll
+            for (int t = 0; t < kMtCh; t++) nc[t] = na + t < nb ? P.child[na + t] : 0;
+        }
+    };
+    auto value = [&](int32_t r, int32_t ch, int32_t sl, int64_t a, int64_t b, const int32_t *c4) {
+        if (ch == j) return sl;
+        int32_t best = -1;
+        for (int64_t t = a; t < b; t++) {
+            const int32_t c = (t - a < kMtCh && c4) ? c4[t - a] : P.child[t];
+            const int32_t x = mring[c & ring_mask];
+            best = max(best, x == n ? -1 : x);
+        }
+        return best < 0 ? n : best;
+    };
+    int32_t lo_next = P.lvl_ptr[0];
+    fetch(0);
+    for (int32_t L = 0; L < P.ell; L++) {
+        const int32_t lo = lo_next, hi = nhi;   // prefetched with the level's first pass
+        lo_next = hi;
+        const int32_t r0 = nr, ch0 = nchain, sl0 = nslot;
+        const int64_t a0 = na, b0 = nb;
+        int32_t c0[kMtCh];
+#pragma unroll
+        for (int t = 0; t < kMtCh; t++) c0[t] = nc[t];
+        fetch(L + 1);   // independent of this level's values: in flight meanwhile
+        if (r0 >= 0) {
+            const int32_t v = value(r0, ch0, sl0, a0, b0, c0);
+            mring[r0 & ring_mask] = v;
+            Mj[r0] = v;
+        }
+        for (int32_t base = lo + 32; base < hi; base += 32) {   // wide levels: further passes
+            const int32_t r = base + lane;
+            if (r < hi) {
+                const int32_t v = value(r, P.chain[r], P.slot[r], P.child_ptr[r], P.child_ptr[r + 1], nullptr);
+                mring[r & ring_mask] = v;
+                Mj[r] = v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_mtable(const DevPoset &P, int32_t *M, cudaStream_t s, int32_t child_reach,
+                          int32_t max_level_width) {
     if (P.k == 0) return cudaSuccess;
+    int ring = 32;
+    while (ring < child_reach + max_level_width + 1) ring <<= 1;
+    if (child_reach >= 0 && ring <= 16384) {   // ring of <= 64 KB per chain
+        const size_t smem = (size_t)ring * 4;
+        cudaError_t e = cudaFuncSetAttribute(k_mtable_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_mtable_ring<<<(unsigned)P.k, 32, smem, s>>>(P, M, ring - 1);
+        COUNT_LAUNCH(1);
+        return cudaGetLastError();
+    }
     const int wpb = 4;
     k_mtable<<<(P.k + wpb - 1) / wpb, 32 * wpb, 0, s>>>(P, M);
     COUNT_LAUNCH(1);

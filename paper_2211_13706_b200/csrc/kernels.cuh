@@ -24,7 +24,11 @@ struct DevPoset {
 };
 
 // ---- kernel (ii): reachability table ----
-cudaError_t launch_mtable(const DevPoset &P, int32_t *M, cudaStream_t s);
+// child_reach = max over DAG edges of rank(parent) - rank(child) (-1:
+// unknown): with the widest level it sizes the shared-memory ring of the
+// fast path; the one-warp-per-chain global-memory sweep otherwise.
+cudaError_t launch_mtable(const DevPoset &P, int32_t *M, cudaStream_t s, int32_t child_reach = -1,
+                          int32_t max_level_width = 0);
 cudaError_t launch_count_nnz(const int32_t *M, int64_t total, int32_t n,
                              unsigned long long *out, cudaStream_t s);
 
