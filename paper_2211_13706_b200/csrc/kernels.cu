@@ -1124,7 +1124,11 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*gen == g0) __nanosleep(32);
+            unsigned rounds = 0;
+            while (*gen == g0) {
+                __nanosleep(32);
+                if (++rounds == (1u << 26)) __trap();   // watchdog (see ptx.cuh)
+            }
         }
         __threadfence();
     }

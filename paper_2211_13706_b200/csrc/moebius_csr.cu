@@ -493,9 +493,10 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks, unsig
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         const unsigned target = (t + 1) * nblocks;
-        unsigned v;
+        unsigned v, rounds = 0;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (++rounds == (1u << 26)) __trap();   // watchdog: a lost arrival faults, not hangs
         } while ((int)(v - target) < 0);
     }
     __syncthreads();
