@@ -38,7 +38,7 @@ PHASES = ("scan", "gather", "perm", "moebius_solve", "chain_diff")
 KERNEL_NAMES = {"scan": "k_scan_tiles+k_scan_carry_tiles (iii)", "gather": "k_gather (iv)",
                 "perm": "k_to_rank_major", "moebius_solve": "k_moeb_* (v)",
                 "chain_diff": "k_chain_diff"}
-MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf", "ringcl"]
+MOEB_NAMES = ["auto", "level", "grid", "warp", "ring", "csr", "ringws", "ringdf", "ringcl", "ringcw"]
 
 
 def parse():
@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--gather-variant", type=int, default=0, help="dense gather kernel for B%%32==0 (tuning)")
     ap.add_argument("--gather-pi-cfg", type=int, default=0, help="gather-order kernel configuration (tuning)")
     ap.add_argument("--ringcl-helpers", type=int, default=0, help="RINGCL helper CTAs (tuning; 0 = auto)")
+    ap.add_argument("--ringcw-sleep", type=int, default=-1, help="RINGCW level-warp poll interval ns (tuning)")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -275,6 +276,8 @@ def main():
         P.set_option("ring_debug", args.ring_debug)
     if args.ringcl_helpers:
         P.set_option("ringcl_helpers", args.ringcl_helpers)
+    if args.ringcw_sleep >= 0:
+        P.set_option("ringcw_sleep", args.ringcw_sleep)
     # strong scaling (default): BASELINE's global batch split over the ranks
     # by columns (no data-path collective); a single function (batch < world)
     # is row-sharded for zeta (NCCL all-gathers, dist.row_sharded_zeta) with

@@ -94,9 +94,13 @@ typedef enum {
                                  publish level completion through mbarriers; far / mid
                                  dependencies are summed levels ahead, near ones on the
                                  critical path                                               */
-    POSET_MOEB_RINGCL = 8     /* RINGDF over a CTA pair (cluster of 2) per column: the second
+    POSET_MOEB_RINGCL = 8,    /* RINGDF over a CTA pair (cluster of 2) per column: the second
                                  SM sums the far dependencies and returns them through
                                  distributed shared memory                  */
+    POSET_MOEB_RINGCW = 9     /* RINGCL with ONE critical warp taking every level's near step
+                                 (no cross-warp hand-off on the dependency chain); the level
+                                 warps hand it g - mid - far in tagged shared-memory records
+                                                                             */
 } poset_moebius_kernel;
 
 typedef struct {
@@ -123,7 +127,7 @@ typedef struct {
     int64_t csr_bytes;    /* bytes of the sparse U-rows (0 = not built)             */
     int64_t zeta_sparse;  /* 1 if zeta gathers over the sparse rows (fill < 1/2)    */
     int64_t ringws;       /* 1 if the RINGWS schedule is available                  */
-    int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGCL available       */
+    int64_t ringdf;       /* bit 0: RINGDF available, bit 1: RINGCL, bit 2: RINGCW  */
     int64_t rdf_bytes;    /* bytes of the RINGDF / RINGCL near + far tables         */
     int64_t ring_bytes;   /* bytes of the RING tables (dist + next slot)            */
     int64_t rws_bytes;    /* bytes of the RINGWS tables                             */
@@ -131,7 +135,11 @@ typedef struct {
                              first loop), the PRAM depth bound of P:L740-745;
                              -1 until poset_set_option("compute_depth_u", 1)   */
     double t_depth;       /* seconds of that computation                            */
-    int64_t gather_bytes; /* bytes of the gather-order table (0 = not built yet)    */
+    int64_t gather_bytes; /* bytes of the gather-order table + delta list (0 = not
+                             built yet)                                             */
+    int64_t gather_entries; /* entries of the zeta delta list (changed niv slots
+                             between consecutive gather positions) */
+    int64_t gather_resets;  /* positions summed from scratch in that list         */
 } poset_info;
 
 /*
@@ -246,8 +254,11 @@ poset_status poset_query(poset_t h, poset_info *out);
  * 4*n*k bytes, is built on the first such call), 1 = lanes over columns,
  * 2 = lanes over ranks, 3 / 4 = rank-order per-lane row reuse with 4 / 2
  * chains per step);
- * "gather_pi_cfg" (process-wide, tuning: configuration of the gather-order
- * kernel, 0 = default, 1..3 = alternatives measured in DESIGN.md §5.2);
+ * "gather_pi_cfg" (process-wide, tuning: 0 = the gather-order kernel with
+ * per-lane row reuse (default), 1..3 = its alternatives measured in
+ * DESIGN.md §5.2, 4 = the delta-list gather: g carried from one gather
+ * position to the next, only the changed chains' rows loaded, with an fp64
+ * error certificate; its list is built on first use -- measured slower);
  * "compute_depth_u" (1: compute D_U now, synchronously, into poset_info.depth_u);
  * "profile" (0/1): record a CUDA event pair on the call's stream around every
  * kernel phase of subsequent calls (see poset_profile_read);

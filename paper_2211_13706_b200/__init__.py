@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = ["Poset", "PosetError", "analyze", "lib", "MOEB_AUTO", "MOEB_LEVEL", "MOEB_GRID", "MOEB_WARP",
            "MOEB_RING", "MOEB_CSR", "MOEB_RINGWS", "MOEB_RINGDF",
-           "MOEB_RINGCL", "LIB_PATH"]
+           "MOEB_RINGCL", "MOEB_RINGCW", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposet.so")
 
@@ -36,8 +36,8 @@ try:
 except OSError as e:   # pragma: no cover
     raise ImportError(f"cannot load {LIB_PATH}: {e} (there is no CPU fallback)") from e
 
-MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS, MOEB_RINGDF, MOEB_RINGCL = (
-    0, 1, 2, 3, 4, 5, 6, 7, 8)
+MOEB_AUTO, MOEB_LEVEL, MOEB_GRID, MOEB_WARP, MOEB_RING, MOEB_CSR, MOEB_RINGWS, MOEB_RINGDF, MOEB_RINGCL, \
+    MOEB_RINGCW = (0, 1, 2, 3, 4, 5, 6, 7, 8, 9)
 _I64, _F64 = 0, 1
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -53,7 +53,8 @@ class PosetInfo(ctypes.Structure):
                 ("reach", _i64), ("dist_bytes", _i64), ("t_dist", ctypes.c_double),
                 ("csr_bytes", _i64), ("zeta_sparse", _i64), ("ringws", _i64), ("ringdf", _i64),
                 ("rdf_bytes", _i64), ("ring_bytes", _i64), ("rws_bytes", _i64),
-                ("depth_u", _i64), ("t_depth", ctypes.c_double), ("gather_bytes", _i64)]
+                ("depth_u", _i64), ("t_depth", ctypes.c_double), ("gather_bytes", _i64),
+                ("gather_entries", _i64), ("gather_resets", _i64)]
 
 
 def _sig(name, args, res=ctypes.c_int):

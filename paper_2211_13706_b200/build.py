@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libposet.so")
-SOURCES = ["api.cu", "kernels.cu", "moebius_ring.cu", "moebius_csr.cu", "moebius_ringws.cu", "moebius_ringdf.cu", "gather_pi.cu", "setup.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "moebius_ring.cu", "moebius_csr.cu", "moebius_ringws.cu", "moebius_ringdf.cu", "gather_pi.cu", "gather_delta.cu", "setup.cpp"]
 HEADERS = ["internal.h", "kernels.cuh", "ptx.cuh", os.path.join("..", "..", "include", "poset.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -53,6 +53,7 @@ struct poset_s {
     unsigned setup_flags = 0;
     GatherPi gpi;                     // batched gather in the per-tile gather order (lazy)
     bool gpi_failed = false;
+    bool gpi_delta_failed = false;
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
     size_t gP_bytes = 0;
     // scratch, grown on demand
@@ -341,7 +342,7 @@ static poset_status finish_setup(poset_s *h) {
                    (h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0) +
                    (h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0);
     I.ringws = h->rws.ok ? 1 : 0;
-    I.ringdf = h->rdf.ok ? (ringcl_fits(h->rdf) ? 3 : 1) : 0;   // bit 1: RINGCL
+    I.ringdf = h->rdf.ok ? (ringcl_fits(h->rdf) ? 3 : 1) | (ringcw_fits(h->rdf) ? 4 : 0) : 0;   // bit 1: RINGCL, 2: RINGCW
     I.ring_bytes = h->ring.ok ? (int64_t)h->ring.npad * (h->ring.kp * 2 + 2) : 0;
     I.rws_bytes = h->rws.ok ? (int64_t)h->rws.npad * h->rws.kp * 2 : 0;
     I.rdf_bytes = h->rdf.ok ? (int64_t)h->rdf.npad * h->rdf.kp * 2 : 0;
@@ -534,8 +535,31 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
             h->gpi_failed = true;
         }
     }
+    // the delta list over the gather order (gather_delta.cu, option
+    // gather_pi_cfg 4; measured slower than the default on C5w / C4w, DESIGN
+    // §5.2), built on first use; if it does not fit, the default kernel serves
+    if (want_pi && h->gpi.ok && !h->gpi.delta_ok && !h->gpi_delta_failed && gather_pi_cfg_get() == 4) {
+        {
+            int32_t *d_off = nullptr;
+            cudaError_t e = cudaMalloc((void **)&d_off, ((size_t)h->H.k + 1) * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(d_off, h->H.chain_off.data(), ((size_t)h->H.k + 1) * 4, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = build_gather_delta(P, d_off, h->gpi, s);
+            cudaFree(d_off);
+            if (e != cudaSuccess) {
+                if (fatal_cuda_error(e)) CK(e);
+                cudaGetLastError();
+                h->gpi_delta_failed = true;
+            }
+        }
+    }
     const bool use_pi = want_pi && h->gpi.ok;
-    h->info.gather_bytes = h->gpi.ok ? (int64_t)h->gpi.npad * (h->H.k + 1) * 4 + (h->gpi.npad / 256) * h->H.k * 8 : 0;
+    const bool use_delta = use_pi && h->gpi.delta_ok && gather_pi_cfg_get() == 4;
+    h->info.gather_bytes = h->gpi.ok ? (int64_t)h->gpi.npad * (h->H.k + 1) * 4 + (h->gpi.npad / 256) * h->H.k * 8
+                                           + h->gpi.nentries * 8 + (h->gpi.npad / 256 + 1) * 8
+                                     : 0;
+    h->info.gather_entries = h->gpi.nentries;
+    h->info.gather_resets = h->gpi.nreset;
     {
         PhaseTimer t(h, POSET_PH_SCAN, s);
         if (B <= 4)   // single pass (decoupled look-back); measured slower than the three-kernel scan for B = 32, 64
@@ -547,6 +571,8 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
         PhaseTimer t(h, POSET_PH_GATHER, s);
         if (h->zeta_csr)
             CK(launch_gather_csr(P, h->csr, dt, h->d_F, g, 0, h->H.n, B, 0, s));
+        else if (use_delta)
+            CK(launch_gather_delta(h->gpi, h->H.n, h->H.k, dt, h->d_F, g, B, h->num_sms, s));
         else if (use_pi)
             CK(launch_gather_pi(h->gpi, h->H.k, dt, h->d_F, g, B, h->num_sms, s));
         else
@@ -579,11 +605,13 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
-    if (which == MOEB_RINGDF || which == MOEB_RINGCL) {
+    if (which == MOEB_RINGDF || which == MOEB_RINGCL || which == MOEB_RINGCW) {
         if (!h->rdf.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
         if (which == MOEB_RINGCL && !ringcl_fits(h->rdf))
             return fail(POSET_EINVAL, "poset_moebius: the RINGCL schedule does not fit this poset; use AUTO");
+        if (which == MOEB_RINGCW && !ringcw_fits(h->rdf))
+            return fail(POSET_EINVAL, "poset_moebius: the RINGCW schedule does not fit this poset; use AUTO");
         st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
         if (st) return st;
         {
@@ -591,7 +619,8 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
             CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
         }
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        if (which == MOEB_RINGCL) {
+        if (which == MOEB_RINGCL || which == MOEB_RINGCW) {
+            h->rdf.cw = which == MOEB_RINGCW;
             cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s);
             if (ce == cudaErrorInvalidConfiguration && h->moeb_opt == MOEB_AUTO) {   // no cluster fits: RINGDF
                 cudaGetLastError();
@@ -837,7 +866,7 @@ poset_status poset_query(poset_t h, poset_info *out) {
 poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
     if (!h || !key) return fail(POSET_EINVAL, "poset_set_option: null argument");
     if (!strcmp(key, "moebius_kernel")) {
-        if (value < MOEB_AUTO || value > MOEB_RINGCL) return fail(POSET_EINVAL, "poset_set_option: bad value");
+        if (value < MOEB_AUTO || value > MOEB_RINGCW) return fail(POSET_EINVAL, "poset_set_option: bad value");
         h->moeb_opt = (int)value;
         return POSET_OK;
     }
@@ -877,13 +906,18 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         h->rdf.dbg = h->ring.dbg;
         return POSET_OK;
     }
+    if (!strcmp(key, "ringcw_sleep")) {   // RINGCW level warps: ns between level polls (tuning)
+        if (value < 0 || value > 100000) return fail(POSET_EINVAL, "poset_set_option: ringcw_sleep is 0..100000");
+        h->rdf.cw_sleep = (int32_t)value;
+        return POSET_OK;
+    }
     if (!strcmp(key, "gather_variant")) {   // process-wide dense-gather kernel choice (tuning)
         if (value < 0 || value > 4) return fail(POSET_EINVAL, "poset_set_option: gather_variant is 0..4");
         set_gather_variant((int)value);
         return POSET_OK;
     }
     if (!strcmp(key, "gather_pi_cfg")) {   // process-wide gather-order kernel configuration (tuning)
-        if (value < 0 || value > 3) return fail(POSET_EINVAL, "poset_set_option: gather_pi_cfg is 0..3");
+        if (value < 0 || value > 4) return fail(POSET_EINVAL, "poset_set_option: gather_pi_cfg is 0..4");
         set_gather_pi_cfg((int)value);
         return POSET_OK;
     }

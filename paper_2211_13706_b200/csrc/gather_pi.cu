@@ -160,6 +160,10 @@ void free_gather_pi(GatherPi &G) {
     if (G.Mg) cudaFree(G.Mg);
     if (G.out_user) cudaFree(G.out_user);
     if (G.Fr) cudaFree(G.Fr);
+    if (G.D) cudaFree(G.D);
+    if (G.Dptr) cudaFree(G.Dptr);
+    if (G.redo) cudaFree(G.redo);
+    if (G.nredo) cudaFree(G.nredo);
     G = GatherPi{};
 }
 
@@ -385,9 +389,12 @@ static cudaError_t gather_pi_t(const GatherPi &G, int32_t k, const void *F, void
     return cudaGetLastError();
 }
 
+int gather_pi_cfg_get() { return g_pi_cfg; }
+
 // cfg (option "gather_pi_cfg", tuning; DESIGN.md §5.2 has the measured
 // table): 0 = 2 chains per step, held indices, round-robin items, L1
-// prefetch of the rows 2 chain groups ahead (default); 1 = as 0, contiguous
+// prefetch of the rows 2 chain groups ahead (default); 4 = the delta-list
+// kernel (gather_delta.cu; its list is built on first use); 1 = as 0, contiguous
 // items + L2 prefetch of the next item's rows; 2 = 2 chains per step, held
 // indices, round-robin, no prefetch (first version); 3 = 4 chains per step,
 // per-step index loads, round-robin

@@ -75,17 +75,35 @@ struct GatherPi {
     int32_t *Mg = nullptr;       // [k][npad] F slots in gather order (n = ∞ / padding)
     int32_t *out_user = nullptr; // [npad] user id of each position (-1 = padding)
     void *Fr = nullptr;          // [npad/256][k] int2 F-slot range per (tile, chain) (L2 prefetch)
+    // delta list (gather_delta.cu): per tile, per position in gather order,
+    // the chains whose niv slot differs from the previous position's
+    bool delta_ok = false;
+    int64_t nentries = 0;        // entries of D
+    int64_t nreset = 0;          // positions summed from scratch (tile starts + magnitude guard)
+    void *D = nullptr;           // [nentries] int2 {new slot | LAST<<31, old slot | RESET<<31}
+    int64_t *Dptr = nullptr;     // [npad/256 + 1] first entry of each tile
+    int64_t *redo = nullptr;     // fp64: (position, column group) pairs to sum directly
+    int64_t redo_cap = 0;
+    unsigned long long *nredo = nullptr;
 };
 cudaError_t build_gather_pi(const DevPoset &P, GatherPi &G, cudaStream_t s);
+// Build the delta list from G.Mg (chain_off: device [k+1]); fails with
+// cudaErrorMemoryAllocation (nothing kept) when it does not fit.
+cudaError_t build_gather_delta(const DevPoset &P, const int32_t *chain_off, GatherPi &G, cudaStream_t s);
+// fp64 also runs k_gather_redo over the positions its error certificate
+// rejected (the redo list is grown here on first use for a batch size).
+cudaError_t launch_gather_delta(GatherPi &G, int32_t n, int32_t k, int dtype, const void *F, void *g,
+                                int64_t B, int num_sms, cudaStream_t s);
 void free_gather_pi(GatherPi &G);
 cudaError_t launch_gather_pi(const GatherPi &G, int32_t k, int dtype, const void *F, void *g, int64_t B,
                              int num_sms, cudaStream_t s);
 int gather_variant_get();
 void set_gather_pi_cfg(int c);   // tuning: kernel configuration of the gather-order kernel
+int gather_pi_cfg_get();         //   0 = default, 1-3 = alternatives, 4 = the delta list
 
 // ---- kernel (v): Moebius U-solve F[slot(r)] = g[user(r)] - Σ_{j≠id} F[M[j][r]] ----
 enum MoebKernel { MOEB_AUTO = 0, MOEB_LEVEL = 1, MOEB_GRID = 2, MOEB_WARP = 3, MOEB_RING = 4, MOEB_CSR = 5,
-                  MOEB_RINGWS = 6, MOEB_RINGDF = 7, MOEB_RINGCL = 8 };
+                  MOEB_RINGWS = 6, MOEB_RINGDF = 7, MOEB_RINGCL = 8, MOEB_RINGCW = 9 };
 int moebius_pick(const DevPoset &P, int64_t batch, int max_level_width, int num_sms);
 cudaError_t launch_moebius_solve(const DevPoset &P, const int32_t *h_lvl_ptr, int dtype,
                                  const void *g, void *F, int64_t batch, int which,
@@ -165,6 +183,9 @@ struct RingDFPlan {
     int32_t wmax = 0;                 // widest level
     int32_t ch_h = 0, nstage_h = 0;   // RINGCL helper staging
     bool cl_ok = false;               // RINGCL fits shared memory
+    bool cw_ok = false;               // RINGCW (critical warp) applies: 4 near entries, <= 3 passes, fits
+    bool cw = false;                  // launch_moebius_ringcl runs the RINGCW variant
+    int32_t cw_sleep = 0;             // RINGCW level warps' poll interval, ns (option ringcw_sleep; 0 = try_wait)
     int32_t nh_max = 1;               // RINGCL helper CTAs per column (1..3) the buffers allow
     int32_t nh_force = 0;             // RINGCL helpers forced (option ringcl_helpers; 0 = auto)
     int32_t nwc = 8;                  // consumer warps
@@ -184,6 +205,7 @@ cudaError_t launch_moebius_ringdf(const DevPoset &P, const RingDFPlan &R, const 
                                   int dtype, const void *gP, void *f, int64_t batch, cudaStream_t s);
 // RINGCL: the same tables over a CTA pair per column (far sums on the second SM)
 bool ringcl_fits(const RingDFPlan &R);
+bool ringcw_fits(const RingDFPlan &R);
 void ringcl_plan(RingDFPlan &R);
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
                                   int dtype, const void *gP, void *f, int64_t batch, int num_sms, cudaStream_t s);

@@ -243,6 +243,7 @@ struct RDFArgs {
     int32_t ring_mask;
     int32_t lg_ch, nstage;
     int32_t lg_chh, nstage_h;   // RINGCL helper staging
+    int32_t cw_sleep;           // RINGCW level warps: ns between level polls (0: try_wait)
     int32_t skip_far;           // timing experiment only (results invalid): bit 0 far, bit 1 mid,
                                 // bit 2 near sums skipped
     unsigned long long *dbg;    // PROF instantiation only: [0] Σ ready->publish, [1] Σ publish->ready
@@ -875,7 +876,7 @@ __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <typename T, int NN, int NM, int FEC, bool PROF = false, int NH = 1>
+template <typename T, int NN, int NM, int FEC, bool PROF = false, int NH = 1, bool CW = false>
 __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     // NH helper CTAs (cluster of NH + 1); the far chunks of a row are split
     // over the 2 * NH helper warps of a level group (chunk c -> c mod 2NH)
@@ -912,12 +913,18 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     T *f = reinterpret_cast<T *>(a.f);
     const unsigned zero_off = (unsigned)RING * 8u;
     __shared__ long long pubt[64];   // instrumentation (a.dbg): owner publish clock per level
+    // CW: hand-off records [8 levels][kNP passes][32 lanes] x 32 bytes after the stages
+    const unsigned hb_base = (stage_base + (unsigned)nstage * sbytes + 15u) & ~15u;
+    static_assert(!CW || NN == 4, "the critical-warp records hold 4 near offsets");
+    if (CW && owner)
+        for (int t = tid; t < 8 * kNP * 256; t += blockDim.x)   // tags 4095 / -1: match no level < 8
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(hb_base + 4u * t), "r"(0xffffffffu) : "memory");
 
     if (tid < 16)
         asm volatile("st.shared.b64 [%0], %1;" ::"r"(ring_base + (unsigned)(RING + tid) * 8), "l"(0ull) : "memory");
     if (tid == 0) {
         for (int s = 0; s < nb; s++) mbar_init(&bars[s], 1);
-        if (owner)   // the owner's level barriers take one arrival per lane
+        if (owner && !CW)   // the owner's level barriers take one arrival per lane (RINGCW: lane 0)
             for (int s = 0; s < kLB; s++) mbar_init(&bars[kMaxStageCL + s], 32);
         for (int i = 0; i < 10; i++) ctrl_p[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -928,7 +935,30 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         if (Ld < 0) return;
         cl_wait_cta(lvl_u32 + (unsigned)(Ld & (kLB - 1)) * 8u, (unsigned)((Ld / kLB) & 1));
     };
-    if (owner && warp == kNWC) {
+    // RINGCW level warps: poll with test_wait and sleep in between, so that
+    // waiting warps do not crowd the shared-memory pipe the critical warp uses
+    auto wait_lvl_sleep = [&](int32_t Ld) {
+        if (Ld < 0) return;
+        const unsigned ad = lvl_u32 + (unsigned)(Ld & (kLB - 1)) * 8u, par = (unsigned)((Ld / kLB) & 1);
+        for (;;) {
+            unsigned ok;
+            asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(ok)
+                         : "r"(ad), "r"(par)
+                         : "memory");
+            if (ok) return;
+            __nanosleep(a.cw_sleep);
+        }
+    };
+    // owner roles.  RINGCW keeps the critical warp alone on its SM
+    // sub-partition (warps 1, 5, 9, 13 share one): warp 1 is the critical
+    // warp, 5 / 9 / 13 idle, the level warps are 0, 2, 3, 4, 6, 7, 8, 10 and
+    // warp 11 the producer.  RINGCL: level warps 0..7, producer 8.
+    constexpr int kCWarp = 1, kProd = CW ? 11 : kNWC;
+    const int mid = !CW ? (warp < kNWC ? warp : -1)
+                        : (warp == 0 ? 0 : warp == 2 ? 1 : warp == 3 ? 2 : warp == 4 ? 3 : warp == 6 ? 4
+                           : warp == 7 ? 5 : warp == 8 ? 6 : warp == 10 ? 7 : -1);
+    if (owner && warp == kProd) {
         // ------------------------------------------------------ producer --
         if (lane == 0) {
             auto issue = [&](int32_t c) {
@@ -1116,11 +1146,95 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         // the owner's last stores into this CTA have landed before it may exit
         for (int32_t X = max(0, a.ell - kNWC); X < a.ell; X++)
             cl_wait(lvl_u32 + (unsigned)(X & (kLB - 1)) * 8u, (unsigned)((X / kLB) & 1));
-    } else if (warp < kNWC) {
+    } else if (CW && warp == kCWarp) {
+        // ------------------------------------------------- critical warp --
+        // Every level's near step in ONE warp (lane = element): no
+        // cross-warp hand-off on the chain.  The owner warps above hand each
+        // level's g - mid - far and near offsets over in tagged 16-byte
+        // records; this warp polls the record (a plain shared load: the tag
+        // and the data are one 16-byte store), adds the <= 4 near values (the
+        // previous two levels, written by this warp), stores F, publishes the
+        // level on lvlbar and forwards F to the helpers.
+        // The loop is kept short (it IS the critical path): one iteration per
+        // 32-element pass, everything it needs in the pass's record (no level
+        // bounds, no branches but the level end), the next record read
+        // during the current pass's near loads.
+        unsigned ln = (unsigned)lane;
+        df_pin(ln);
+        const unsigned my_rec = hb_base + ln * 32u, rb = ring_base;
+        unsigned lvlb = lvl_u32, ctl = ctrl + 4;
+        df_pin(lvlb);
+        df_pin(ctl);
+        const int32_t ell = a.ell;
+        auto rec_ok = [](const uint4 &h0, const uint4 &h1, int32_t L) {
+            const unsigned ez = ((unsigned)L & 7u) | (((unsigned)L >> 3) & 7u) << 16;
+            const unsigned ew = (((unsigned)L >> 6) & 7u) | (((unsigned)L >> 9) & 7u) << 16;
+            return ((h0.z & 0x70007u) == ez) & ((h0.w & 0x70007u) == ew) & (h1.z == (unsigned)L);
+        };
+        auto wait_rec = [&](unsigned ad, int32_t L, uint4 &h0, uint4 &h1) {
+            for (unsigned spins = 0;; spins++) {
+                if (spins > (1u << 28)) __trap();   // watchdog: a lost record is POSET_ECUDA, not a hang
+                h0 = df_lds128(ad);
+                h1 = df_lds128(ad + 16u);
+                if (__all_sync(0xffffffffu, rec_ok(h0, h1, L))) return;
+            }
+        };
+        const long long tstart = a.dbg ? clock64() : 0;
+        unsigned long long nwait = 0;
+        int32_t L = 0;
+        unsigned ellu = (unsigned)ell;
+        df_pin(ellu);
+        const int32_t ellr = (int32_t)ellu;
+        unsigned cur = my_rec;
+        uint4 h0, h1;
+        if (ellr > 0) wait_rec(cur, 0, h0, h1);
+        const unsigned is0 = ln == 0 ? 1u : 0u;
+        while (L < ellr) {
+            // (1) near loads of this pass (addresses from the record in registers)
+            const T v0 = bits_to<T>(df_lds64(rb + (h0.z & 0xfff8u)));
+            const T v1 = bits_to<T>(df_lds64(rb + ((h0.z >> 16) & 0xfff8u)));
+            const T v2 = bits_to<T>(df_lds64(rb + (h0.w & 0xfff8u)));
+            const T v3 = bits_to<T>(df_lds64(rb + ((h0.w >> 16) & 0xfff8u)));
+            // (2) the next pass's record (level L+1 after the last pass of L)
+            const unsigned last = (h1.x >> 17) & 1u;   // warp-uniform
+            const int32_t Ln = L + (int32_t)last;
+            const unsigned nxt = last ? hb_base + (unsigned)(Ln & 7) * (kNP * 1024u) + ln * 32u : cur + 1024u;
+            const uint4 n0 = df_lds128(nxt), n1 = df_lds128(nxt + 16u);
+            // (3) off-chain arithmetic while the loads fly
+            const unsigned barad = lvlb + (unsigned)(L & (kLB - 1)) * 8u, pub = last & is0;
+            const unsigned ez = ((unsigned)Ln & 7u) | (((unsigned)Ln >> 3) & 7u) << 16;
+            const unsigned ew = (((unsigned)Ln >> 6) & 7u) | (((unsigned)Ln >> 9) & 7u) << 16;
+            const T gsv = bits_to<T>(((u64)h0.y << 32) | h0.x);
+            // (4) the chain: F = g - mid - far - near, into the ring
+            const T Fx = gsv - ((v0 + v1) + (v2 + v3));
+            df_stp64(rb + (h1.x & 0xffffu), df_bits<T>(Fx), h1.x & (1u << 16));
+            __syncwarp();   // the lanes' F stores before lane 0's release and this warp's next loads
+            asm volatile(
+                "{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\n"
+                "@q mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n"
+                "@q st.relaxed.cta.shared.s32 [%1], %2;\n}" ::"r"(barad),
+                "r"(ctl), "r"(h1.y), "r"(pub)
+                : "memory");
+            L = Ln;
+            h0 = n0;
+            h1 = n1;
+            cur = nxt;
+            const bool ok = ((n0.z & 0x70007u) == ez) & ((n0.w & 0x70007u) == ew) & (n1.z == (unsigned)Ln);
+            if (__builtin_expect(!__all_sync(0xffffffffu, ok | (Ln >= ellr)), 0)) {   // not handed over yet
+                wait_rec(cur, L, h0, h1);
+                nwait++;
+            }
+        }
+        if (a.dbg && b == 0 && ln == 0) {
+            atomicAdd(a.dbg + 0, nwait);
+            atomicAdd(a.dbg + 2, (unsigned long long)ell);
+            atomicAdd(a.dbg + 4, (unsigned long long)(clock64() - tstart));
+        }
+    } else if (mid >= 0) {
         // --------------------------------------------------- owner warps --
         int32_t cb = 0;
         auto ld_bounds = [&](int32_t i0, int32_t &vlo, int32_t &vhi) {
-            const int32_t L = warp + (i0 + lane) * kNWC;
+            const int32_t L = mid + (i0 + lane) * kNWC;
             vlo = a.lvl_ptr[min(L, a.ell)];
             vhi = a.lvl_ptr[min(L + 1, a.ell)];
         };
@@ -1128,7 +1242,7 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
         ld_bounds(0, clo, chi);
         int32_t staged = 0;
         for (int32_t i = 0;; i++) {
-            const int32_t L = warp + i * kNWC;
+            const int32_t L = mid + i * kNWC;
             if (L >= a.ell) break;
             if (i - cb == 32) {
                 cb += 32;
@@ -1171,6 +1285,35 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         for (int q = 0; q < NN / 2; q++) nw[p][q] = zero_off | (zero_off << 16);
                     }
                 }
+                const bool mprof = CW && a.dbg != nullptr && b == 0 && lane == 0;
+                const long long m0 = mprof ? clock64() : 0;
+                long long m1 = m0, t2 = 0, t2b = 0, rtt = 0;
+                if constexpr (CW) {
+                    // RINGCW: everything that does not need levels L-6 .. L-3 first
+                    // (far partials, the mid row words), then one wait and the mid
+                    // sum in a single round of loads: the latency from level L-3's
+                    // completion to this level's record is what paces the critical warp
+                    t2 = clock64();
+                    cl_wait(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, (unsigned)((L / kLB) & 1));
+                    t2b = clock64();
+                    uint4 mw[NPX][NM / 8];
+#pragma unroll
+                    for (int p = 0; p < NPX; p++) {
+                        sp[p] = T(0);
+                        if (act(p)) {
+#pragma unroll
+                            for (int k2 = 0; k2 < 2 * NH; k2++)
+                                sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + ((lo + 32 * p + lane) & (SB - 1))) * 8u));
+#pragma unroll
+                            for (int q = 0; q < NM / 8; q++) mw[p][q] = df_lds128(rowa[p] + 16u * q);
+                        }
+                    }
+                    if (a.cw_sleep) wait_lvl_sleep(L - kNear - 1); else wait_lvl(L - kNear - 1);   // mid: levels <= L-3
+                    m1 = mprof ? clock64() : 0;
+#pragma unroll
+                    for (int p = 0; p < NPX; p++)
+                        if (act(p) && !(a.skip_far & 2)) sp[p] += df_sum_w<T, NM>(ring_base, mw[p]);
+                } else {
                 wait_lvl(L - kNear - 1);   // mid: levels <= L-3
 #pragma unroll
                 for (int p = 0; p < NPX; p++) {
@@ -1183,16 +1326,17 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                     }
                 }
                 // far sums of this level, from the helper (as late as possible)
-                const long long t2 = PROF ? clock64() : 0;
+                t2 = PROF ? clock64() : 0;
                 cl_wait(far_u32 + (unsigned)(L & (kLB - 1)) * 8u, (unsigned)((L / kLB) & 1));
-                const long long t2b = PROF ? clock64() : 0;
-                const long long rtt = PROF && L >= kMid + 1 ? t2b - pubt[(L - kMid - 1) & 63] : 0;
+                t2b = PROF ? clock64() : 0;
+                rtt = PROF && L >= kMid + 1 ? t2b - pubt[(L - kMid - 1) & 63] : 0;
 #pragma unroll
                 for (int p = 0; p < NPX; p++)
                     if (act(p))
 #pragma unroll
                         for (int k2 = 0; k2 < 2 * NH; k2++)
                             sp[p] += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + ((lo + 32 * p + lane) & (SB - 1))) * 8u));
+                }
                 unsigned lvl_addr = lvl_u32 + (unsigned)(L & (kLB - 1)) * 8u;
                 df_pin(lvl_addr);
                 T gs[NPX], Fx[NPX];
@@ -1213,80 +1357,127 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
                         df_pin(na[p][2 * q + 1]);
                     }
                 }
-                const long long t3 = PROF ? clock64() : 0;
-                wait_lvl(L - 1);   // near: the critical path
-                if (PROF && b == 0 && lane == 0) {
-                    const long long t4 = clock64();
-                    atomicAdd(a.dbg + 0, (unsigned long long)(t2b - t2));
-                    atomicAdd(a.dbg + 1, (unsigned long long)(t4 - t3));
-                    atomicAdd(a.dbg + 2, (unsigned long long)rtt);
-                    atomicAdd(a.dbg + 3, 1ull);
-                }
-                T v[NPX][NN];
+                if constexpr (CW) {
+                    // hand the level to the critical warp, one 32-byte record per
+                    // lane and pass: {g - mid - far, near offsets | tag bits},
+                    // {ring offset | on << 16 | last pass << 17, hi, L, 0}; each
+                    // 16-byte half is one store carrying the tag
+                    const unsigned ez = (L & 7u) | (((unsigned)L >> 3) & 7u) << 16;
+                    const unsigned ew = (((unsigned)L >> 6) & 7u) | (((unsigned)L >> 9) & 7u) << 16;
+                    const unsigned hbL = hb_base + (unsigned)(L & 7) * (kNP * 1024u) + (unsigned)lane * 32u;
+                    const int npl = (hi - lo + 31) >> 5;
 #pragma unroll
-                for (int p = 0; p < NPX; p++)
+                    for (int p = 0; p < NPX; p++)
+                        if (act(p)) {
+                            const u64 gb = df_bits<T>(gs[p]);
+                            const int32_t e = lo + 32 * p + lane;
+                            const unsigned w4 = (unsigned)(e & a.ring_mask) * 8u | (e < hi ? 1u << 16 : 0u) |
+                                                (p == npl - 1 ? 1u << 17 : 0u);
+                            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(hbL + 1024u * p + 16u),
+                                         "r"(w4), "r"(hi), "r"(L), "r"(0u)
+                                         : "memory");
+                            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(hbL + 1024u * p),
+                                         "r"((unsigned)gb), "r"((unsigned)(gb >> 32)), "r"(nw[p][0] | ez),
+                                         "r"(nw[p][1] | ew)
+                                         : "memory");
+                        }
+                    // outputs once the critical warp has completed level L
+                    const long long m3 = mprof ? clock64() : 0;
+                    if (a.cw_sleep) wait_lvl_sleep(L); else wait_lvl(L);
+                    if constexpr (CW) {   // forward F to the helpers' rings (their lvlbar[L % kLB])
 #pragma unroll
-                    for (int j = 0; j < NN; j++) v[p][j] = bits_to<T>(df_lds64(na[p][j]));
+                        for (unsigned r = 1; r <= NH; r++) {
+                            const unsigned rbar = cl_mapa(lvl_addr, r);
 #pragma unroll
-                for (int p = 0; p < NPX; p++) {
-#pragma unroll
-                    for (int st = 1; st < NN; st <<= 1)
-#pragma unroll
-                        for (int j = 0; j < NN; j += 2 * st) v[p][j] += v[p][j + st];
-                    Fx[p] = gs[p] - v[p][0];
-                }
-#pragma unroll
-                for (int p = 0; p < NPX; p++) df_stp64(sa[p], df_bits<T>(Fx[p]), stp[p]);
-                if (NPX == kNP) {
-                    // passes beyond kNP: serially, all deps done (far sums in sfar)
-                    for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
-                        const int32_t e = base + lane;
-                        const int32_t ee = e < hi ? e : base;
-                        const unsigned st = stage_base + ((unsigned)(ee >> lgc) % ns) * sbytes;
-                        const unsigned off = (unsigned)(ee & (ch - 1));
-                        const unsigned row = st + off * (unsigned)a.kpn * 2;
-                        const T g1 = bits_to<T>(df_lds64(st + nbytes + off * 8));
-                        int32_t u1;
-                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + nbytes + gbytes + off * 4));
-                        const unsigned p16 = lds32u(row + OFF_PN) & 0xffffu;
-                        T sf1 = T(0);
-#pragma unroll
-                        for (int k2 = 0; k2 < 2 * NH; k2++)
-                            sf1 += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + (ee & (SB - 1))) * 8u));
-                        const T s1 = sf1 +
-                                     df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
-                        const T F1 = g1 - s1;
-                        if (e < hi) {
-                            const unsigned sl = ring_base + (unsigned)(e & a.ring_mask) * 8u;
-                            asm volatile("st.shared.b64 [%0], %1;" ::"r"(sl), "l"(df_bits<T>(F1)) : "memory");
-#pragma unroll
-                            for (unsigned r = 1; r <= NH; r++) cl_st_async64(cl_mapa(sl, r), df_bits<T>(F1), cl_mapa(lvl_addr, r));
-                            f[(size_t)u1 * a.B + b] = F1 - bits_to<T>(df_lds64(ring_base + p16));
+                            for (int p = 0; p < NPX; p++)
+                                if (stp[p]) cl_st_async64(cl_mapa(sa[p], r), df_lds64(sa[p]), rbar);
                         }
                     }
-                }
-                // publish locally (critical path): all 32 lanes arrive
-                asm volatile(
-                    "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
-                    "mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
-                    "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
-                    "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
-                    : "memory");
-                if (PROF && lane == 0) pubt[L & 63] = clock64();
-                // forward F to the helper's ring: each store completes its bytes
-                // on the helper's lvlbar[L % kLB] (armed there with 8 * width)
-                {
-#pragma unroll
-                    for (unsigned r = 1; r <= NH; r++) {
-                        const unsigned rbar = cl_mapa(lvl_addr, r);
-#pragma unroll
-                        for (int p = 0; p < NPX; p++)
-                            if (stp[p]) cl_st_async64(cl_mapa(sa[p], r), df_bits<T>(Fx[p]), rbar);
+                    if (mprof) {
+                        const long long m4 = clock64();
+                        atomicAdd(a.dbg + 6, (unsigned long long)(m4 - m3));
+                        atomicAdd(a.dbg + 7, (unsigned long long)(m3 - m1));
                     }
-                }
 #pragma unroll
-                for (int p = 0; p < NPX; p++)
-                    if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
+                    for (int p = 0; p < NPX; p++)
+                        if (stp[p])
+                            f[(size_t)u[p] * a.B + b] = bits_to<T>(df_lds64(sa[p])) - bits_to<T>(df_lds64(ring_base + pn[p]));
+                } else {
+                    const long long t3 = PROF ? clock64() : 0;
+                    wait_lvl(L - 1);   // near: the critical path
+                    if (PROF && b == 0 && lane == 0) {
+                        const long long t4 = clock64();
+                        atomicAdd(a.dbg + 0, (unsigned long long)(t2b - t2));
+                        atomicAdd(a.dbg + 1, (unsigned long long)(t4 - t3));
+                        atomicAdd(a.dbg + 2, (unsigned long long)rtt);
+                        atomicAdd(a.dbg + 3, 1ull);
+                    }
+                    T v[NPX][NN];
+    #pragma unroll
+                    for (int p = 0; p < NPX; p++)
+    #pragma unroll
+                        for (int j = 0; j < NN; j++) v[p][j] = bits_to<T>(df_lds64(na[p][j]));
+    #pragma unroll
+                    for (int p = 0; p < NPX; p++) {
+    #pragma unroll
+                        for (int st = 1; st < NN; st <<= 1)
+    #pragma unroll
+                            for (int j = 0; j < NN; j += 2 * st) v[p][j] += v[p][j + st];
+                        Fx[p] = gs[p] - v[p][0];
+                    }
+    #pragma unroll
+                    for (int p = 0; p < NPX; p++) df_stp64(sa[p], df_bits<T>(Fx[p]), stp[p]);
+                    if (NPX == kNP) {
+                        // passes beyond kNP: serially, all deps done (far sums in sfar)
+                        for (int32_t base = lo + 32 * kNP; base < hi; base += 32) {
+                            const int32_t e = base + lane;
+                            const int32_t ee = e < hi ? e : base;
+                            const unsigned st = stage_base + ((unsigned)(ee >> lgc) % ns) * sbytes;
+                            const unsigned off = (unsigned)(ee & (ch - 1));
+                            const unsigned row = st + off * (unsigned)a.kpn * 2;
+                            const T g1 = bits_to<T>(df_lds64(st + nbytes + off * 8));
+                            int32_t u1;
+                            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(u1) : "r"(st + nbytes + gbytes + off * 4));
+                            const unsigned p16 = lds32u(row + OFF_PN) & 0xffffu;
+                            T sf1 = T(0);
+    #pragma unroll
+                            for (int k2 = 0; k2 < 2 * NH; k2++)
+                                sf1 += bits_to<T>(df_lds64(sfar_base + (unsigned)(k2 * SB + (ee & (SB - 1))) * 8u));
+                            const T s1 = sf1 +
+                                         df_sum<T, NM>(ring_base, row) + df_sum_u16<T, NN>(ring_base, row + OFF_NEAR);
+                            const T F1 = g1 - s1;
+                            if (e < hi) {
+                                const unsigned sl = ring_base + (unsigned)(e & a.ring_mask) * 8u;
+                                asm volatile("st.shared.b64 [%0], %1;" ::"r"(sl), "l"(df_bits<T>(F1)) : "memory");
+    #pragma unroll
+                                for (unsigned r = 1; r <= NH; r++) cl_st_async64(cl_mapa(sl, r), df_bits<T>(F1), cl_mapa(lvl_addr, r));
+                                f[(size_t)u1 * a.B + b] = F1 - bits_to<T>(df_lds64(ring_base + p16));
+                            }
+                        }
+                    }
+                    // publish locally (critical path): all 32 lanes arrive
+                    asm volatile(
+                        "{\n.reg .pred q;\nsetp.eq.u32 q, %0, 0;\n"
+                        "mbarrier.arrive.release.cta.shared::cta.b64 _, [%1];\n"
+                        "@q st.relaxed.cta.shared.s32 [%2], %3;\n}" ::"r"(lane),
+                        "r"(lvl_addr), "r"(ctrl + 4), "r"(hi)
+                        : "memory");
+                    if (PROF && lane == 0) pubt[L & 63] = clock64();
+                    // forward F to the helper's ring: each store completes its bytes
+                    // on the helper's lvlbar[L % kLB] (armed there with 8 * width)
+                    {
+    #pragma unroll
+                        for (unsigned r = 1; r <= NH; r++) {
+                            const unsigned rbar = cl_mapa(lvl_addr, r);
+    #pragma unroll
+                            for (int p = 0; p < NPX; p++)
+                                if (stp[p]) cl_st_async64(cl_mapa(sa[p], r), df_bits<T>(Fx[p]), rbar);
+                        }
+                    }
+    #pragma unroll
+                    for (int p = 0; p < NPX; p++)
+                        if (stp[p]) f[(size_t)u[p] * a.B + b] = Fx[p] - bits_to<T>(df_lds64(ring_base + pn[p]));
+                }
             };
             if (np <= 1)
                 level(std::integral_constant<int, 1>{});
@@ -1298,15 +1489,17 @@ __global__ void __launch_bounds__(32 * kNWH) k_moeb_ringcl(RDFArgs a) {
     cl_sync();   // neither CTA exits while its peer may still write into its shared memory
 }
 
-static size_t ringcl_smem_bytes(const RingDFPlan &R) {   // owner stages; the helper stages nothing
+static size_t ringcl_smem_bytes(const RingDFPlan &R, bool cw = false) {   // owner stages; the helper stages nothing
     const size_t so = (size_t)R.nstage * R.ch * ((size_t)R.kpn * 2 + 12);
-    return (size_t)(3 * R.ring + 16) * 8 + 8 * (size_t)(kMaxStageCL + 2 * kLB) + 48 + so;
+    return (size_t)(3 * R.ring + 16) * 8 + 8 * (size_t)(kMaxStageCL + 2 * kLB) + 48 + so +
+           (cw ? 16 + (size_t)8 * kNP * 1024 : 0);   // RINGCW hand-off records
 }
 
 void ringcl_plan(RingDFPlan &R) {
     R.ch_h = R.ch;
     R.nstage_h = R.nstage;
     R.cl_ok = R.ok && R.fe <= 128 && ringcl_smem_bytes(R) <= kSmemCapDF;
+    R.cw_ok = R.cl_ok && R.nn == 4 && R.wmax <= 32 * kNP && ringcl_smem_bytes(R, true) <= kSmemCapDF;
     // helper CTAs: 2 NH far-sum buffers of RING >> {0,1,2} entries, each
     // holding >= 10 level widths (the helpers run <= 8 levels ahead)
     R.nh_max = 1;
@@ -1315,6 +1508,7 @@ void ringcl_plan(RingDFPlan &R) {
 }
 
 bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
+bool ringcw_fits(const RingDFPlan &R) { return R.cw_ok; }
 
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
                                   int dtype, const void *gP, void *f, int64_t B, int num_sms, cudaStream_t s) {
@@ -1325,7 +1519,7 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     if (R.nh_max >= 2 && 3 * B <= num_sms) nh = 2;
     if (R.nh_force > 0) nh = std::min(R.nh_force, R.nh_max);   // tuning option ringcl_helpers
     if (P.n == 0) return cudaSuccess;
-    if (!ringcl_fits(R)) return cudaErrorInvalidConfiguration;
+    if (!ringcl_fits(R) || (R.cw && !ringcw_fits(R))) return cudaErrorInvalidConfiguration;
     RDFArgs a{};
     a.Dn = R.D;
     a.Df = R.D + R.npad * R.kpn;
@@ -1349,10 +1543,19 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     a.nstage_h = R.nstage_h;
     a.dbg = R.prof ? R.dbg : nullptr;   // ring_debug bit 3: wait-time counters
     a.skip_far = R.skip_far;            // timing experiments only
-    const size_t smem = ringcl_smem_bytes(R);
+    a.cw_sleep = R.cw_sleep;
+    const size_t smem = ringcl_smem_bytes(R, R.cw);
     void *fn = nullptr;
+#define RCW_FN(NM, FEC)                                                                        \
+    if (R.cw && R.nn == 4 && R.nm == NM && fec == FEC)                                         \
+        fn = nh == 3 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, 4, NM, FEC, false, 3, true>    \
+                                   : (void *)k_moeb_ringcl<double, 4, NM, FEC, false, 3, true>) \
+           : nh == 2 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, 4, NM, FEC, false, 2, true>    \
+                                   : (void *)k_moeb_ringcl<double, 4, NM, FEC, false, 2, true>) \
+                     : (dtype == 0 ? (void *)k_moeb_ringcl<u64, 4, NM, FEC, false, 1, true>    \
+                                   : (void *)k_moeb_ringcl<double, 4, NM, FEC, false, 1, true>);
 #define RCL_FN(NN, NM, FEC)                                                                    \
-    if (R.nn == NN && R.nm == NM && fec == FEC)                                                \
+    if (!R.cw && R.nn == NN && R.nm == NM && fec == FEC)                                       \
         fn = R.prof ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, true>              \
                                   : (void *)k_moeb_ringcl<double, NN, NM, FEC, true>)          \
            : nh == 3 ? (dtype == 0 ? (void *)k_moeb_ringcl<u64, NN, NM, FEC, false, 3>         \
@@ -1365,6 +1568,8 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
 #define RCL_FE(FEC) RCL_NM(4, FEC) RCL_NM(8, FEC) RCL_NM(16, FEC)
     const int fec = R.fe <= 64 ? 4 : R.fe <= 96 ? 6 : 8;   // chunks per row, split by parity
     RCL_FE(4) RCL_FE(6) RCL_FE(8)
+    RCW_FN(16, 4) RCW_FN(16, 6) RCW_FN(16, 8) RCW_FN(32, 4) RCW_FN(32, 6) RCW_FN(32, 8)
+#undef RCW_FN
 #undef RCL_FE
 #undef RCL_NM
 #undef RCL_FN
@@ -1372,7 +1577,7 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    const int cdim = R.prof ? 2 : nh + 1;   // the instrumented build is the 1-helper kernel
+    const int cdim = R.prof && !R.cw ? 2 : nh + 1;   // the instrumented build is the 1-helper kernel
     cfg.gridDim = dim3((unsigned)(cdim * B));
     cfg.blockDim = dim3(32 * kNWH);
     cfg.dynamicSmemBytes = smem;

@@ -22,7 +22,7 @@ from oracle import brute  # noqa: E402
 from oracle.chain import ChainOracle, zeta_sampled_edges  # noqa: E402
 
 KERNELS = [pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP, pz.MOEB_RING, pz.MOEB_CSR, pz.MOEB_RINGWS,
-           pz.MOEB_RINGDF, pz.MOEB_RINGCL]
+           pz.MOEB_RINGDF, pz.MOEB_RINGCL, pz.MOEB_RINGCW]
 
 
 def kernels_for(P):
@@ -32,7 +32,7 @@ def kernels_for(P):
     return [k for k in KERNELS
             if (k != pz.MOEB_RING or info["dist_bytes"] > 0) and (k != pz.MOEB_CSR or info["csr_bytes"] > 0)
             and (k != pz.MOEB_RINGWS or info["ringws"]) and (k != pz.MOEB_RINGDF or info["ringdf"] & 1)
-            and (k != pz.MOEB_RINGCL or info["ringdf"] & 2)]
+            and (k != pz.MOEB_RINGCL or info["ringdf"] & 2) and (k != pz.MOEB_RINGCW or info["ringdf"] & 4)]
 facts = load_facts()
 PAPER_CHAINS = [[int(v) - 1 for v in c.split(",")] for c in facts["chains"].split(";")]
 
@@ -216,7 +216,8 @@ def test_ring_schedule_selection_and_limits():
     P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
     info = P.info()
     assert info["dist_bytes"] > 0 and 0 < info["reach"] < 65535
-    assert info["moebius_kernel"] == pz.MOEB_RINGCL and info["ringws"] == 1 and info["ringdf"] == 3
+    assert info["moebius_kernel"] in (pz.MOEB_RINGCL, pz.MOEB_RINGCW) and info["ringws"] == 1
+    assert info["ringdf"] & 3 == 3
     for B in (1, 2, 7, 33):
         f = W.int_values(n, B, -1000, 1000, seed=B)
         g = gpu_zeta(P, f)
@@ -231,6 +232,8 @@ def test_ring_schedule_selection_and_limits():
         for nh in (1, 2, 3):   # helper CTAs per column (cluster of nh + 1)
             P.set_option("ringcl_helpers", nh)
             assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), (B, nh)
+            if info["ringdf"] & 4:
+                assert (gpu_moebius(P, h, pz.MOEB_RINGCW) == want).all(), (B, nh)
         P.set_option("ringcl_helpers", 0)
         for lpe in (1, 2, 4, 8):
             P.set_option("ring_lpe", lpe)
@@ -278,6 +281,8 @@ def test_ring_schedules_wide_levels_and_large_batch(wide):
         assert (gpu_moebius(P, h, pz.MOEB_RINGDF) == want).all(), B
         if info["ringdf"] & 2:
             assert (gpu_moebius(P, h, pz.MOEB_RINGCL) == want).all(), B
+        if info["ringdf"] & 4:
+            assert (gpu_moebius(P, h, pz.MOEB_RINGCW) == want).all(), B
 
     h = W.int_values(n, 80, -10**17, 10**17, seed=11)   # 2 x 80 CTAs > 148 SMs
     assert (gpu_moebius(P, h) == O.moebius(h)).all()
@@ -323,21 +328,26 @@ def test_dense_gather_variants(variant):
         P.set_option("gather_variant", 0)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_gather_order_configs(cfg):
-    """The gather-order kernel's configurations (option gather_pi_cfg)
-    against O2, bit-exact int64 and fp64 within the tolerance, with ∞
-    entries (the bottom of the poset) and a ragged tile."""
+    """The gather-order kernel's configurations (option gather_pi_cfg; 4 is
+    the delta-list gather) against O2, bit-exact int64 and fp64 within the
+    tolerance, with ∞ entries (the bottom of the poset), a ragged tile and
+    1, 2 and 4 columns per lane (B = 32, 64, 96, 128)."""
     n = 7003
     src, dst = W.window_dag(n, 2, 64, 9, forced=True)
     P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
     P.set_option("gather_pi_cfg", cfg)
     try:
-        for B in (32, 64):
+        for B in (32, 64, 96, 128):
             f = W.int_values(n, B, -10**15, 10**15, seed=B + cfg)
             assert (gpu_zeta(P, f) == O.zeta(f)).all(), B
             ff = W.normal_values(n, B, seed=B + 2)
             assert_fp64_close(gpu_zeta(P, ff), O.zeta(ff), O.zeta(np.abs(ff)))
+            # 16 decades of magnitude: the delta list's carried sums fail its
+            # error certificate at many positions (the direct re-sum path)
+            fw = ff * 10.0 ** np.random.default_rng(B).uniform(-8, 8, size=ff.shape)
+            assert_fp64_close(gpu_zeta(P, fw), O.zeta(fw), O.zeta(np.abs(fw)))
     finally:
         P.set_option("gather_pi_cfg", 0)
 
