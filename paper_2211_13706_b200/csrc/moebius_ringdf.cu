@@ -1515,8 +1515,11 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     // two helper CTAs per column when three SMs per column fit one wave
     // (measured on C5w: 1 helper 128.0 ms, 2 helpers 100.4, 3 helpers 103.7;
     // three stay available through the ringcl_helpers option)
+    // (round 2, C5w B = 32: 3 helpers 94.9 ms vs 96.9 for int64, but 102.4 vs
+    // 100.7 for fp64 -- so int64 takes three when four SMs per column fit)
     int nh = 1;
     if (R.nh_max >= 2 && 3 * B <= num_sms) nh = 2;
+    if (R.nh_max >= 3 && dtype == 0 && 4 * B <= num_sms) nh = 3;
     if (R.nh_force > 0) nh = std::min(R.nh_force, R.nh_max);   // tuning option ringcl_helpers
     if (P.n == 0) return cudaSuccess;
     if (!ringcl_fits(R) || (R.cw && !ringcw_fits(R))) return cudaErrorInvalidConfiguration;
