@@ -294,6 +294,14 @@ def main():
         cols = (0, wl.batch) if row_mode else pdist.column_shard(wl.batch, world, rank)
         f_host = np.ascontiguousarray(f_all[:, cols[0]:cols[1]])
         del f_all
+    shard = None
+    if row_mode:
+        # row-sharded index: each rank keeps its 4·k·n/G
+        # bytes of table rows (D_U first: it needs the whole table)
+        P.set_option("compute_depth_u", 1)
+        slo, shi = pdist.shard_index(P)
+        shard = {"rows": [slo, shi], "index_bytes_per_rank": P.info()["table_bytes"],
+                 "index_bytes_unsharded": 4 * info["n"] * info["k"]}
     B = f_host.shape[1]
     x = torch.from_numpy(f_host).cuda()
     g = torch.empty_like(x)
@@ -384,7 +392,8 @@ def main():
                  "unit": "GB/s", "frac": kernels["gather"]["frac"], "traffic": zt, "traffic_source": zsrc}
     if dom == "moebius_solve":
         try:
-            P.set_option("compute_depth_u", 1)
+            if P.info()["depth_u"] < 0:
+                P.set_option("compute_depth_u", 1)
             du = P.info()["depth_u"]
         except pz.PosetError:   # sparse-rows poset: D_U needs the dense table
             du = None
@@ -516,7 +525,7 @@ def main():
                        "reach": info["reach"],
                        "parallelism": (f"zeta row-shard x{world} + NCCL all-gather, Möbius on rank 0"
                                        if row_mode else f"column-shard x{world}"),
-                       "depth_u": P.info()["depth_u"], "provenance": prov,
+                       "depth_u": P.info()["depth_u"], "provenance": prov, "index_shard": shard,
                        "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
             "gbs_per_step": sum(ab[p] for p in kernels) / (ms_max / args.steps / 1e3) / 1e9,
             # nnz(N)·B per second: the work the method needs;

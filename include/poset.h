@@ -222,6 +222,20 @@ poset_status poset_scan_carry(poset_t h, void *F, const void *carry_in, int64_t 
                               int64_t slot_hi, int64_t batch, poset_dtype dt, void *stream);
 poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t row_lo,
                                int64_t row_hi, int64_t batch, poset_dtype dt, void *stream);
+/*
+ * poset_shard_rows -- keep only index rows [row_lo, row_hi) (rank order) of the
+ * dense table on this handle: 4*k*(row_hi - row_lo) bytes instead of 4*n*k
+ * (the row-sharded index of SURVEY §8(f) N3; the setup still built the whole
+ * table, this frees it).  Afterwards poset_gather_rows accepts only rows in
+ * that range, poset_zeta / LEVEL / GRID / WARP Möbius / compute_depth_u /
+ * poset_export_mtable return EINVAL; the ring and sparse-row Möbius schedules
+ * keep working unless flags has POSET_SHARD_DROP_MOEBIUS (frees their tables
+ * too: for ranks that never run the Möbius solve).  Synchronises the device.
+ * Errors: EINVAL (bad range, sparse-row zeta, already sharded), ENOMEM, ECUDA.
+ */
+#define POSET_SHARD_DROP_MOEBIUS 1u
+poset_status poset_shard_rows(poset_t h, int64_t row_lo, int64_t row_hi, uint32_t flags);
+
 /* carry_out[b] = value of the segmented prefix of tails_all[0..rank-1]
  * (device [world][2][batch] as written by poset_scan_slots on each rank), the
  * carry into rank `rank`'s slot range. */

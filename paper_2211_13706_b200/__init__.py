@@ -84,6 +84,7 @@ _sig("poset_debug_read", [_vp, _vp])
 _sig("poset_destroy", [_vp], None)
 _sig("poset_strerror", [ctypes.c_int], ctypes.c_char_p)
 _sig("poset_last_error", [], ctypes.c_char_p)
+_sig("poset_shard_rows", [_vp, _i64, _i64, ctypes.c_uint32])
 _sig("poset_abi_version", [], ctypes.c_int)
 _sig("poset_sync", [_vp, _vp])
 
@@ -290,6 +291,10 @@ class Poset:
         B = F.shape[1] if F.ndim == 2 else 1
         _check(lib.poset_gather_rows(self._h, _ptr(F), _ptr(g_rank), lo, hi, B, _dtype_code(F),
                                      _stream_ptr(stream, F)))
+
+    def shard_rows(self, lo, hi, drop_moebius=False):
+        """Keep only the index rows [lo, hi) on this handle (poset_shard_rows)."""
+        _check(lib.poset_shard_rows(self._h, int(lo), int(hi), 1 if drop_moebius else 0))
 
     def combine_tails(self, tails_all, world, rank, carry, stream=None):
         B = carry.shape[-1]

@@ -53,6 +53,9 @@ struct poset_s {
     unsigned setup_flags = 0;
     GatherPi gpi;                     // batched gather in the per-tile gather order (lazy)
     bool gpi_failed = false;
+    // poset_shard_rows: only index rows [m_lo, m_hi) kept (d_M is then [k][m_hi - m_lo])
+    bool sharded = false;
+    int64_t m_lo = 0, m_hi = 0;
     bool gpi_delta_failed = false;
     void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
     size_t gP_bytes = 0;
@@ -82,7 +85,8 @@ struct poset_s {
         P.child_ptr = d_child_ptr;
         P.child = d_child;
         P.slot_user = d_slot_user;
-        P.M = d_M;
+        P.M = sharded ? d_M - m_lo : d_M;
+        P.ldm = sharded ? m_hi - m_lo : H.n;
         return P;
     }
 };
@@ -510,6 +514,8 @@ struct PhaseTimer {
 typedef poset_status (*device_fn)(poset_s *, const void *, void *, int64_t, int, cudaStream_t);
 
 static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int dt, cudaStream_t s) {
+    if (h->sharded)
+        return fail(POSET_EINVAL, "poset_zeta: the index rows are sharded (poset_shard_rows); use the split phases");
     poset_status st = ensure_F(h, B, s);
     if (st) return st;
     st = grow(h, &h->d_scan, &h->scan_bytes, std::max(scan_scratch_bytes(h->H.n, B), scan1p_scratch_bytes(h->H.n, B)));
@@ -593,6 +599,9 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
                 : h->ring.ok ? MOEB_RING
                 : h->csr.ok  ? MOEB_CSR
                              : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+    if (h->sharded && (which == MOEB_LEVEL || which == MOEB_GRID || which == MOEB_WARP))
+        return fail(POSET_EINVAL, "poset_moebius: the index rows are sharded (poset_shard_rows); the LEVEL / "
+                                  "GRID / WARP schedules read the whole table");
     if (h->sparse_only && which != MOEB_CSR)
         return fail(POSET_EINVAL, "poset_moebius: sparse-rows poset (no dense table): only the CSR schedule "
                                   "applies; use AUTO");
@@ -776,6 +785,8 @@ poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t l
     poset_status st = check_call(h, F, g_rank, batch, dt, "poset_gather_rows");
     if (st) return st;
     if (lo < 0 || hi > h->H.n || lo > hi) return fail(POSET_EINVAL, "poset_gather_rows: bad range");
+    if (h->sharded && hi > lo && (lo < h->m_lo || hi > h->m_hi))
+        return fail(POSET_EINVAL, "poset_gather_rows: rows outside the kept shard (poset_shard_rows)");
     CK(cudaSetDevice(h->device));
     if ((st = check_split("poset_gather_rows", {F, g_rank}))) return st;
     cudaStream_t s = (cudaStream_t)stream;
@@ -791,6 +802,49 @@ poset_status poset_gather_rows(poset_t h, const void *F, void *g_rank, int64_t l
     }
     CK(launch_gather(h->dev(), dt, F, g_rank, lo, hi, batch, 1, pb ? h->d_part : nullptr, h->num_sms, s));
     return end_call(h, s, POSET_OK);
+}
+
+poset_status poset_shard_rows(poset_t h, int64_t lo, int64_t hi, uint32_t flags) {
+    if (!h) return fail(POSET_EINVAL, "poset_shard_rows: null handle");
+    const HostPoset &H = h->H;
+    if (lo < 0 || hi > H.n || lo > hi) return fail(POSET_EINVAL, "poset_shard_rows: bad range");
+    if (h->sparse_only || h->zeta_csr || !h->d_M)
+        return fail(POSET_EINVAL, "poset_shard_rows: the zeta of this poset does not gather from the dense table");
+    if (h->sharded) return fail(POSET_EINVAL, "poset_shard_rows: already sharded");
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());   // no call may still read the whole table
+    const int64_t w = hi - lo;
+    int32_t *Mc = nullptr;
+    cudaError_t e = cudaMalloc((void **)&Mc, std::max<size_t>((size_t)w * H.k * 4, 4));
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(POSET_ENOMEM, "poset_shard_rows: no room for the kept rows");
+    }
+    CK(e);
+    if (w > 0 && H.k > 0)
+        CK(cudaMemcpy2D(Mc, (size_t)w * 4, h->d_M + lo, (size_t)H.n * 4, (size_t)w * 4, (size_t)H.k,
+                        cudaMemcpyDeviceToDevice));
+    CK(cudaDeviceSynchronize());
+    cudaFree(h->d_M);
+    h->d_M = Mc;
+    h->sharded = true;
+    h->m_lo = lo;
+    h->m_hi = hi;
+    free_gather_pi(h->gpi);     // built from the whole table; zeta is refused from now on
+    h->gpi_failed = true;
+    if (flags & POSET_SHARD_DROP_MOEBIUS) {   // ranks that never run the Möbius solve
+        void *ptrs[] = {h->ring.D, h->ring.Pn, h->rws.D, h->rdf.D, h->csr.ptr, h->csr.idx};
+        for (void *p : ptrs)
+            if (p) cudaFree(p);
+        h->ring.D = nullptr; h->ring.Pn = nullptr; h->rws.D = nullptr; h->rdf.D = nullptr;
+        h->csr.ptr = nullptr; h->csr.idx = nullptr;
+        h->ring.ok = h->rws.ok = h->rdf.ok = h->csr.ok = false;
+        h->rdf.cl_ok = h->rdf.cw_ok = false;
+        h->info.dist_bytes = h->info.ring_bytes = h->info.rws_bytes = h->info.rdf_bytes = h->info.csr_bytes = 0;
+        h->info.ringws = h->info.ringdf = 0;
+    }
+    h->info.table_bytes = w * H.k * 4;
+    return POSET_OK;
 }
 
 poset_status poset_combine_tails(poset_t h, const void *tails_all, int64_t world, int64_t rank,
@@ -922,7 +976,8 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "compute_depth_u")) {
-        if (h->sparse_only) return fail(POSET_EINVAL, "compute_depth_u: needs the dense table (sparse-rows poset)");
+        if (h->sparse_only || h->sharded)
+            return fail(POSET_EINVAL, "compute_depth_u: needs the whole dense table (sparse-rows or sharded poset)");
         CK(cudaSetDevice(h->device));
         double t0 = now_seconds();
         int32_t *d_sr = nullptr, *d_D = nullptr;
@@ -993,6 +1048,7 @@ poset_status poset_debug_read(poset_t h, int64_t *out8) {
 
 poset_status poset_export_mtable(poset_t h, int32_t *out) {
     if (!h || !out) return fail(POSET_EINVAL, "poset_export_mtable: null argument");
+    if (h->sharded) return fail(POSET_EINVAL, "poset_export_mtable: the index rows are sharded");
     const HostPoset &H = h->H;
     if (h->sparse_only) {   // from the U-rows: own chain = pos(x), the rest from the row, ∞ = -1
         std::vector<int64_t> ptr((size_t)H.n + 1);

@@ -667,7 +667,7 @@ cudaError_t launch_combine_tails(int dtype, const void *tails, int64_t world, in
 // loads are L1 broadcasts.  Block id: column-group block fastest, then
 // j-slice, then rank tile.
 template <typename T, int CB, int VEC, int U>
-__global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, int32_t n, int32_t k,
+__global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, int32_t n, int32_t k, int64_t ldm,
                                                 const T *__restrict__ F, T *__restrict__ out,
                                                 const int32_t *__restrict__ rank_user,
                                                 int64_t row_lo, int64_t row_hi, int32_t B, int GB,
@@ -691,12 +691,12 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t *__restrict__ M, i
     const T *Fc = F + c0;
     int32_t idx[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) idx[u] = (j0 + u < j1) ? __ldg(Mr + (size_t)(j0 + u) * n) : n;
+    for (int u = 0; u < U; u++) idx[u] = (j0 + u < j1) ? __ldg(Mr + (size_t)(j0 + u) * ldm) : n;
     for (int j = j0; j < j1; j += U) {
         int32_t nidx[U];
 #pragma unroll
         for (int u = 0; u < U; u++)
-            nidx[u] = (j + U + u < j1) ? __ldg(Mr + (size_t)(j + U + u) * n) : n;
+            nidx[u] = (j + U + u < j1) ? __ldg(Mr + (size_t)(j + U + u) * ldm) : n;
 #pragma unroll
         for (int u = 0; u < U; u++) {
             T v[CB];
@@ -758,7 +758,7 @@ __device__ __forceinline__ void head_loads8(const char *Fb, unsigned rowbytes, c
 
 template <typename T, int KCH>
 __global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restrict__ M, int32_t n,
-                                                        int32_t k, const T *__restrict__ F,
+                                                        int32_t k, int64_t ldm, const T *__restrict__ F,
                                                         T *__restrict__ out,
                                                         const int32_t *__restrict__ rank_user,
                                                         int64_t row_lo, int64_t row_hi, int32_t B,
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(256, 2) k_gather_cols(const int32_t *__restric
             const int w = i * 32 + lane, jj = w / TR, t = w % TR;
             const int64_t r = r0 + t;
             if (j0 + jj < k && r < row_hi)
-                cp_async4(&S[jj][t], M + (size_t)(j0 + jj) * n + r);
+                cp_async4(&S[jj][t], M + (size_t)(j0 + jj) * ldm + r);
             else
                 S[jj][t] = n;   // the zero row of F
         }
@@ -856,7 +856,7 @@ __device__ __forceinline__ void ld4_if_ne(u64 (&v)[4], const void *p, int32_t a,
 
 template <typename T, int KCH, int KC = 4, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) k_gather_r4(const int32_t *__restrict__ M, int32_t n,
-                                                      int32_t k, const T *__restrict__ F,
+                                                      int32_t k, int64_t ldm, const T *__restrict__ F,
                                                       T *__restrict__ out,
                                                       const int32_t *__restrict__ rank_user,
                                                       int64_t row_lo, int64_t row_hi, int32_t B,
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_r4(const int32_t *__restri
             const int w = i * 32 + lane, jj = w / TRW, t = w % TRW;
             const int64_t r = r0 + t;
             if (j0 + jj < k && r < row_hi)
-                cp_async4(&S[t][jj], M + (size_t)(j0 + jj) * n + r);
+                cp_async4(&S[t][jj], M + (size_t)(j0 + jj) * ldm + r);
             else
                 S[t][jj] = n;   // the zero row of F
         }
@@ -1007,7 +1007,7 @@ static cudaError_t gather_launch(const DevPoset &P, const void *F, void *g, int6
     const int64_t blocks = tiles * S * GB;
     void *dst = S > 1 ? partial : g;
     int m = S > 1 ? 2 : mode;
-    k_gather<T, CB, VEC, U><<<(unsigned)blocks, 256, 0, s>>>(P.M, P.n, P.k, (const T *)F, (T *)dst,
+    k_gather<T, CB, VEC, U><<<(unsigned)blocks, 256, 0, s>>>(P.M, P.n, P.k, P.ldm, (const T *)F, (T *)dst,
                                                              P.rank_user, lo, hi, (int32_t)B, GB, WG,
                                                              S, m);
     COUNT_LAUNCH(S > 1 ? 2 : 1);
@@ -1029,10 +1029,10 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
         const int64_t tiles = (hi - lo + 8 * 16 - 1) / (8 * 16);
         if (gather_variant() != 3)   // 2 chains per step: fewer registers, 3 CTAs per SM (measured best)
             k_gather_r4<T, 64, 2, 3><<<(unsigned)(tiles * G32), 256, 0, s>>>(
-                P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+                P.M, P.n, P.k, P.ldm, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         else
             k_gather_r4<T, 64><<<(unsigned)(tiles * G32), 256, 0, s>>>(
-                P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+                P.M, P.n, P.k, P.ldm, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         COUNT_LAUNCH(1);
         return cudaGetLastError();
     }
@@ -1041,7 +1041,7 @@ static cudaError_t gather_t(const DevPoset &P, const void *F, void *g, int64_t l
         const int G32 = (int)(B / 32);
         const int64_t tiles = (hi - lo + 8 * TR - 1) / (8 * TR);
         k_gather_cols<T, KCH><<<(unsigned)(tiles * G32), 256, 0, s>>>(
-            P.M, P.n, P.k, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
+            P.M, P.n, P.k, P.ldm, (const T *)F, (T *)g, P.rank_user, lo, hi, (int32_t)B, G32, mode);
         COUNT_LAUNCH(1);
         return cudaGetLastError();
     }

@@ -21,6 +21,8 @@ struct DevPoset {
     const int32_t *child;       // [m]
     const int32_t *slot_user;   // [n]  slot -> user | start flag (bit 31)
     const int32_t *M;           // [k][n] chain-major slot table (n = none)
+    int64_t ldm = 0;            // row stride of M (n; hi - lo after poset_shard_rows, M then
+                                // points lo entries before the kept rows)
 };
 
 // ---- kernel (ii): reachability table ----

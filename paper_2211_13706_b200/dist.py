@@ -87,11 +87,27 @@ def row_sharded_zeta(P, f, group=None, out=None):
     return out.reshape(f.shape)
 
 
+def shard_index(P, group=None, rank=None, world=None):
+    """Keep only this rank's index rows (``poset_shard_rows``): 4·k·n/G bytes
+    per rank instead of 4·n·k.  Rank 0 keeps the Möbius
+    tables (single-function Möbius runs there); the others drop them."""
+    if rank is None or world is None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo, hi, _ = shard_range(P.n, world, rank)
+    P.shard_rows(lo, hi, drop_moebius=rank != 0)
+    return lo, hi
+
+
 def emulate_row_sharded_zeta(P, f, world: int):
     """The call sequence of ``row_sharded_zeta`` for ``world`` emulated ranks
     on one GPU; each collective becomes a copy.  For tests only -- no kernel
-    waits on another."""
+    waits on another.  ``P`` is one handle for every rank, or a list of
+    ``world`` handles of the same poset (e.g. each with its rows sharded by
+    ``shard_index``): rank p's calls then go to ``P[p]``."""
     import torch
+    Ps = list(P) if isinstance(P, (list, tuple)) else [P] * world
+    P = Ps[0]
     n = P.n
     f2 = f.reshape(n, -1)
     B = f2.shape[1]
@@ -100,19 +116,19 @@ def emulate_row_sharded_zeta(P, f, world: int):
     tails = torch.zeros((world, 2, B), dtype=f.dtype, device=f.device)
     for p in range(world):
         lo, hi, _ = shard_range(n, world, p)
-        P.scan_slots(f2, F, tails[p], lo, hi)
+        Ps[p].scan_slots(f2, F, tails[p], lo, hi)
     for p in range(world):
         lo, hi, _ = shard_range(n, world, p)
         carry = torch.zeros((B,), dtype=f.dtype, device=f.device)
-        P.combine_tails(tails, world, p, carry)
-        P.scan_carry(F, carry, lo, hi)
+        Ps[p].combine_tails(tails, world, p, carry)
+        Ps[p].scan_carry(F, carry, lo, hi)
     F[n].zero_()
     g_rank = torch.zeros((world * chunk, B), dtype=f.dtype, device=f.device)
     for p in range(world):
         lo, hi, _ = shard_range(n, world, p)
         if hi > lo:
             part = torch.zeros((chunk, B), dtype=f.dtype, device=f.device)
-            P.gather_rows(F, part, lo, hi)
+            Ps[p].gather_rows(F, part, lo, hi)
             g_rank[p * chunk:(p + 1) * chunk] = part
     out = torch.empty_like(f2)
     P.rank_to_user(g_rank[:n].contiguous(), out)

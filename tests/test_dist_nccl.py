@@ -54,6 +54,12 @@ def _worker(rank, world, port, q):
         back = P.moebius(g)
         torch.cuda.synchronize()
         ok &= bool((g.cpu().numpy() == O.zeta(f)[:, lo:hi]).all()) and bool(torch.equal(back, x))
+        # the row-sharded index: each rank keeps only its rows, same result
+        pdist.shard_index(P)
+        f = W.int_values(n, 2, -10**15, 10**15, seed=6)
+        g = pdist.row_sharded_zeta(P, torch.from_numpy(f).cuda())
+        torch.cuda.synchronize()
+        ok &= bool((g.cpu().numpy() == O.zeta(f)).all())
         dist.destroy_process_group()
         q.put((rank, ok, ""))
     except Exception as e:   # pragma: no cover

@@ -421,6 +421,40 @@ def test_split_phase_row_sharded_zeta(G):
             assert_fp64_close(got, O.zeta(f), O.zeta(np.abs(f)))
 
 
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_index_rows(G):
+    """The row-sharded index (poset_shard_rows): each of G
+    handles keeps only its 4·k·n/G bytes of rows; the split-phase zeta over
+    the G handles matches O2, rows outside a shard and the whole-table calls
+    are refused, rank 0 keeps its Möbius tables, the others drop them."""
+    from paper_2211_13706_b200 import dist
+    n = 30011
+    src, dst = W.window_dag(n, 2, 200, 5, forced=True)
+    O = ChainOracle(n, src, dst)
+    Ps = [pz.Poset(n, src, dst) for _ in range(G)]
+    k = Ps[0].k
+    for p, P in enumerate(Ps):
+        lo, hi = dist.shard_index(P, rank=p, world=G)
+        assert P.info()["table_bytes"] == 4 * k * (hi - lo)
+    for dtype, B in (("i64", 1), ("i64", 32), ("f64", 3)):
+        f = W.int_values(n, B, -10**12, 10**12, 2) if dtype == "i64" else W.normal_values(n, B, 2)
+        got = host(dist.emulate_row_sharded_zeta(Ps, dev(f), G))
+        if dtype == "i64":
+            assert (got == O.zeta(f)).all(), B
+        else:
+            assert_fp64_close(got, O.zeta(f), O.zeta(np.abs(f)))
+    F = torch.zeros((n + 1, 1), dtype=torch.int64, device="cuda")
+    g = torch.zeros((n, 1), dtype=torch.int64, device="cuda")
+    with pytest.raises(pz.PosetError):
+        Ps[0].gather_rows(F, g, 0, n)            # beyond rank 0's rows
+    with pytest.raises(pz.PosetError):
+        Ps[0].zeta(dev(W.int_values(n, 1, -5, 5, 1)))
+    h = W.int_values(n, 2, -10**15, 10**15, 4)
+    assert (gpu_moebius(Ps[0], h) == O.moebius(h)).all()   # rank 0 keeps the ring tables
+    with pytest.raises(pz.PosetError):
+        Ps[1].moebius(dev(h))
+
+
 # ------------------------------------------------------------ full sizes
 #
 # The configs bench.py times, at full size, compared ELEMENT BY ELEMENT with
