@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--ringcl-helpers", type=int, default=0, help="RINGCL helper CTAs (tuning; 0 = auto)")
     ap.add_argument("--ringcw-sleep", type=int, default=-1, help="RINGCW level-warp poll interval ns (tuning)")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
     ap.add_argument("--no-e2e", action="store_true")
