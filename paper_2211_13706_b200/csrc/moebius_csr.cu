@@ -485,6 +485,27 @@ cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, co
 }
 
 // ------------------------------------------------------ Möbius (CSR) ------
+// Level L+1's row entries are one contiguous index range; while level L is
+// summed, thread 0 of every CTA pulls its 1/gridDim share of that range into
+// L2 (cp.async.bulk.prefetch: no registers, nothing waits on it), so the
+// next level's index loads are L2 hits instead of DRAM round trips.
+__device__ __forceinline__ void prefetch_next_rows(const DevPoset &P, const int64_t *__restrict__ ptr,
+                                                   const int32_t *__restrict__ idx, int32_t L) {
+    if (threadIdx.x != 0 || L + 1 >= P.ell) return;
+    const int64_t a = ptr[P.lvl_ptr[L + 1]], b = ptr[P.lvl_ptr[L + 2]];
+    if ((b - a) * 4 > ((int64_t)32 << 20)) return;   // a wide level's rows would only evict L2
+    const int64_t per = ((b - a) + gridDim.x - 1) / gridDim.x;
+    int64_t e0 = a + per * blockIdx.x, e1 = min(b, e0 + per);
+    if (e1 <= e0) return;
+    uintptr_t p0 = reinterpret_cast<uintptr_t>(idx + e0) & ~(uintptr_t)15;
+    const uintptr_t p1 = (reinterpret_cast<uintptr_t>(idx + e1) + 15) & ~(uintptr_t)15;
+    while (p0 < p1) {
+        const unsigned n = (unsigned)(p1 - p0 < ((uintptr_t)1 << 16) ? p1 - p0 : ((uintptr_t)1 << 16));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(n) : "memory");
+        p0 += n;
+    }
+}
+
 // Grid barrier on a monotone arrival counter: barrier number t completes when
 // the counter reaches (t + 1) * nblocks.  One release-add per CTA and an
 // acquire spin by one thread; no reset, no generation flag.
@@ -516,6 +537,9 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks, unsig
 // WPI (warps per item slot) follows the average row length: 8 for the
 // long rows of C2 / C3w / C4w, 4 for medium rows, 1 (a warp per element, no
 // slot barrier) for the short rows of the paper's ER DAGs.
+#ifndef CSR_COLS_U
+#define CSR_COLS_U 8
+#endif
 template <typename T, bool COLS, int kCsrWPI>
 __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t *__restrict__ ptr,
                                                       const int32_t *__restrict__ idx,
@@ -529,6 +553,7 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t 
     const int64_t my_slot = (int64_t)blockIdx.x * kCsrSlots + slot;
     for (int32_t L = 0; L < P.ell; L++) {
         const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        prefetch_next_rows(P, ptr, idx, L);
         const int64_t items = (int64_t)(hi - lo) * G;
         // every slot runs the same number of rounds (named barriers inside)
         const int64_t rounds = (items + nslots - 1) / nslots;
@@ -543,13 +568,17 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t 
                 cg = (int)(it % G);
                 a = ptr[r];
                 b = ptr[r + 1];
+                if (ws == 0) {   // the epilogue's addresses, loaded before the row sum
+                    my = __ldg(P.slot + r);
+                    u = __ldg(P.rank_user + r);
+                }
             }
             // this warp's chunk of the row
             const int64_t len = b - a, per = (len + kCsrWPI - 1) / kCsrWPI;
             const int64_t ca = a + min(len, per * ws), cb = a + min(len, per * (ws + 1));
             if (COLS) {
                 const int col = cg * 32 + lane;
-                const T s = valid ? row_sum_cols<T, true, 8>(idx, ca, cb, F, B, col) : T(0);
+                const T s = valid ? row_sum_cols<T, true, CSR_COLS_U>(idx, ca, cb, F, B, col) : T(0);
                 part[slot][ws][lane] = s;
             } else {
                 // B % 32 != 0: lanes over entries, one column of the group at
@@ -565,18 +594,19 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr(DevPoset P, const int64_t 
             if (kCsrWPI > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
             else __syncwarp();
             if (ws == 0 && valid) {
-                my = P.slot[r];
-                u = P.rank_user[r];
-                const bool has_prev = !(P.slot_user[my] < 0);   // bit 31 = chain start
                 const int ncol = COLS ? 32 : min(B - cg * 32, 32);
                 if (lane < ncol) {
+                    // three independent loads (one round of latency), then the sums
                     const int col = cg * 32 + lane;
+                    const bool has_prev = !(__ldg(P.slot_user + my) < 0);   // bit 31 = chain start
+                    const T gx = __ldg(g + (size_t)u * B + col);
+                    const T fp = ld_cg(F + (size_t)(my > 0 ? my - 1 : 0) * B + col);
                     T s = part[slot][0][lane];
 #pragma unroll
                     for (int w2 = 1; w2 < kCsrWPI; w2++) s += part[slot][w2][lane];
-                    const T Fx = __ldg(g + (size_t)u * B + col) - s;
+                    const T Fx = gx - s;
                     F[(size_t)my * B + col] = Fx;
-                    f[(size_t)u * B + col] = has_prev ? Fx - ld_cg(F + (size_t)(my - 1) * B + col) : Fx;
+                    f[(size_t)u * B + col] = has_prev ? Fx - fp : Fx;
                 }
             }
             if (kCsrWPI > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * kCsrWPI) : "memory");
@@ -598,11 +628,13 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr_thread(DevPoset P, const i
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int32_t L = 0; L < P.ell; L++) {
         const int32_t lo = P.lvl_ptr[L], hi = P.lvl_ptr[L + 1];
+        prefetch_next_rows(P, ptr, idx, L);
         const int64_t items = (int64_t)(hi - lo) * B;
         for (int64_t it = tid; it < items; it += nth) {
             const int32_t r = lo + (int32_t)(it / B);
             const int c = (int)(it % B);
             const int64_t a = ptr[r], b = ptr[r + 1];
+            const int32_t my = __ldg(P.slot + r), usr = __ldg(P.rank_user + r);   // epilogue addresses, early
             constexpr int U = 8;
             T acc[U];
 #pragma unroll
@@ -620,10 +652,12 @@ __global__ void __launch_bounds__(1024, 1) k_moeb_csr_thread(DevPoset P, const i
             for (int st = 1; st < U; st <<= 1)
 #pragma unroll
                 for (int u = 0; u < U; u += 2 * st) acc[u] += acc[u + st];
-            const int32_t my = P.slot[r], usr = P.rank_user[r];
-            const T Fx = __ldg(g + (size_t)usr * B + c) - acc[0];
+            const bool start = __ldg(P.slot_user + my) < 0;
+            const T gx = __ldg(g + (size_t)usr * B + c);
+            const T fp = ld_cg(F + (size_t)(my > 0 ? my - 1 : 0) * B + c);
+            const T Fx = gx - acc[0];
             F[(size_t)my * B + c] = Fx;
-            f[(size_t)usr * B + c] = P.slot_user[my] < 0 ? Fx : Fx - ld_cg(F + (size_t)(my - 1) * B + c);
+            f[(size_t)usr * B + c] = start ? Fx : Fx - fp;
         }
         if (L + 1 < P.ell) grid_sync(bar, gridDim.x, (unsigned)L);
     }
