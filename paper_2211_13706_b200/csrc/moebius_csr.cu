@@ -489,9 +489,25 @@ cudaError_t launch_gather_csr(const DevPoset &P, const CsrRows &C, int dtype, co
 // summed, thread 0 of every CTA pulls its 1/gridDim share of that range into
 // L2 (cp.async.bulk.prefetch: no registers, nothing waits on it), so the
 // next level's index loads are L2 hits instead of DRAM round trips.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *lo, const void *hi) {
+    uintptr_t p0 = reinterpret_cast<uintptr_t>(lo) & ~(uintptr_t)15;
+    const uintptr_t p1 = (reinterpret_cast<uintptr_t>(hi) + 15) & ~(uintptr_t)15;
+    while (p0 < p1) {
+        const unsigned n = (unsigned)(p1 - p0 < ((uintptr_t)1 << 16) ? p1 - p0 : ((uintptr_t)1 << 16));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(n) : "memory");
+        p0 += n;
+    }
+}
 __device__ __forceinline__ void prefetch_next_rows(const DevPoset &P, const int64_t *__restrict__ ptr,
                                                    const int32_t *__restrict__ idx, int32_t L) {
     if (threadIdx.x != 0 || L + 1 >= P.ell) return;
+    const int32_t r0 = P.lvl_ptr[L + 1], r1 = P.lvl_ptr[L + 2];
+    if (blockIdx.x == 0 && r1 - r0 <= 8192) {   // a narrow next level's row pointers, slots, user ids
+        // (narrow levels are latency-bound; a wide one hides the latency itself)
+        bulk_prefetch_l2(ptr + r0, ptr + r1 + 1);
+        bulk_prefetch_l2(P.slot + r0, P.slot + r1);
+        bulk_prefetch_l2(P.rank_user + r0, P.rank_user + r1);
+    }
     const int64_t a = ptr[P.lvl_ptr[L + 1]], b = ptr[P.lvl_ptr[L + 2]];
     if ((b - a) * 4 > ((int64_t)32 << 20)) return;   // a wide level's rows would only evict L2
     const int64_t per = ((b - a) + gridDim.x - 1) / gridDim.x;
