@@ -945,6 +945,12 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         }
         return POSET_OK;
     }
+    if (!strcmp(key, "ringcl_chunk")) {   // RINGCL owner stage chunk, ranks (tuning; 0 = the plan's)
+        if (value != 0 && value != 32 && value != 64 && value != 128 && value != 256)
+            return fail(POSET_EINVAL, "ringcl_chunk is 0, 32, 64, 128 or 256");
+        h->rdf.ch_cl = (int32_t)value;
+        return POSET_OK;
+    }
     if (!strcmp(key, "ringcl_helpers")) {   // RINGCL helper CTAs per column (tuning; 0 = auto)
         if (value < 0 || value > 3) return fail(POSET_EINVAL, "ringcl_helpers is 0..3");
         h->rdf.nh_force = (int32_t)value;

@@ -190,6 +190,7 @@ struct RingDFPlan {
     int32_t cw_sleep = 0;             // RINGCW level warps' poll interval, ns (option ringcw_sleep; 0 = try_wait)
     int32_t nh_max = 1;               // RINGCL helper CTAs per column (1..3) the buffers allow
     int32_t nh_force = 0;             // RINGCL helpers forced (option ringcl_helpers; 0 = auto)
+    int32_t ch_cl = 0;                // RINGCL owner stage chunk (option ringcl_chunk; 0 = the plan's)
     int32_t nwc = 8;                  // consumer warps
     bool prof = false;                // instrumented instantiation (tuning)
     int32_t skip_far = 0;             // timing experiment only

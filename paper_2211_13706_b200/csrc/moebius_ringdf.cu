@@ -1523,6 +1523,16 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
     if (R.nh_force > 0) nh = std::min(R.nh_force, R.nh_max);   // tuning option ringcl_helpers
     if (P.n == 0) return cudaSuccess;
     if (!ringcl_fits(R) || (R.cw && !ringcw_fits(R))) return cudaErrorInvalidConfiguration;
+    if (R.ch_cl > 0 && R.ch_cl != R.ch) {   // tuning: another owner stage chunk (same tables)
+        RingDFPlan R2 = R;
+        R2.ch = R.ch_cl;
+        R2.ch_h = R.ch_cl;
+        R2.nstage = std::max(2, (int)(((int64_t)(kNWC + 1) * R.wmax + R.ch_cl - 1) / R.ch_cl) + 1);
+        R2.nstage_h = R2.nstage;
+        R2.ch_cl = 0;
+        if (R2.nstage > kMaxStageCL || ringcl_smem_bytes(R2, R2.cw) > kSmemCapDF) return cudaErrorInvalidValue;
+        return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s);
+    }
     RDFArgs a{};
     a.Dn = R.D;
     a.Df = R.D + R.npad * R.kpn;
