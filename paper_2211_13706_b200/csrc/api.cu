@@ -977,7 +977,7 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "gather_pi_cfg")) {   // process-wide gather-order kernel configuration (tuning)
-        if (value < 0 || value > 4) return fail(POSET_EINVAL, "poset_set_option: gather_pi_cfg is 0..4");
+        if (value < 0 || value > 7) return fail(POSET_EINVAL, "poset_set_option: gather_pi_cfg is 0..7");
         set_gather_pi_cfg((int)value);
         return POSET_OK;
     }

@@ -197,8 +197,8 @@ __device__ __forceinline__ u64 as_bits<double>(double x) { return (u64)__double_
 // into L2 the F rows the CTA's NEXT item reads (cp.async.bulk.prefetch, one
 // contiguous slot range per chain), so first touches of F rows do not stall
 // the dependent reuse walk on DRAM latency.
-template <typename T, int KC, int MINB, bool STEP_IDS, int PFD>
-__global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restrict__ Mg, int64_t npad,
+template <typename T, int KC, int MINB, bool STEP_IDS, int PFD, int RP = RPL>
+__global__ void __launch_bounds__(32 * GT / (4 * RP), MINB) k_gather_pi(const int32_t *__restrict__ Mg, int64_t npad,
                                                          int32_t k, const T *__restrict__ F,
                                                          T *__restrict__ out,
                                                          const int32_t *__restrict__ out_user, int32_t B,
@@ -237,15 +237,15 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
         if (nstages > 1) issue(1);
     }
     const unsigned rowbytes = (unsigned)B * sizeof(T);
-    const int pos0 = warp * 32 + q * RPL;   // this lane's first position in the tile
-    T acc[RPL][4];
+    const int pos0 = warp * (4 * RP) + q * RP;   // this lane's first position in the tile
+    T acc[RP][4];
     for (int64_t s = 0; s < nstages; s++) {
         const int c = (int)(s % nchunk);
         const int64_t it = ilo + (s / nchunk) * istep;
         const int cg = (int)(it % G32);
         if (c == 0) {
 #pragma unroll
-            for (int t = 0; t < RPL; t++)
+            for (int t = 0; t < RP; t++)
 #pragma unroll
                 for (int i = 0; i < 4; i++) acc[t][i] = T(0);
         }
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
                     for (int i = 0; i < 4; i++) v[u][i] = 0;
                 }
 #pragma unroll
-                for (int t = 0; t < RPL; t++) {
+                for (int t = 0; t < RP; t++) {
                     int32_t id[KC];
 #pragma unroll
                     for (int u = 0; u < KC; u++) id[u] = jj + u < jn ? S[(jj + u) * GT + t] : -1;
@@ -299,17 +299,18 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
             }
         } else
         for (int jj = 0; jj < jn; jj += KC) {
-            int32_t id[KC][RPL];
+            int32_t id[KC][RP];
 #pragma unroll
             for (int u = 0; u < KC; u++) {
                 if (jj + u < jn) {
-                    const int4 a = *reinterpret_cast<const int4 *>(S + (jj + u) * GT);
-                    const int4 b = *reinterpret_cast<const int4 *>(S + (jj + u) * GT + 4);
-                    id[u][0] = a.x; id[u][1] = a.y; id[u][2] = a.z; id[u][3] = a.w;
-                    id[u][4] = b.x; id[u][5] = b.y; id[u][6] = b.z; id[u][7] = b.w;
+#pragma unroll
+                    for (int h = 0; h < RP / 4; h++) {
+                        const int4 a = *reinterpret_cast<const int4 *>(S + (jj + u) * GT + 4 * h);
+                        id[u][4 * h] = a.x; id[u][4 * h + 1] = a.y; id[u][4 * h + 2] = a.z; id[u][4 * h + 3] = a.w;
+                    }
                 } else {
 #pragma unroll
-                    for (int t = 0; t < RPL; t++) id[u][t] = -1;   // no chain: never loads
+                    for (int t = 0; t < RP; t++) id[u][t] = -1;   // no chain: never loads
                 }
             }
             if (PFD > 0 && jj + PFD * KC < jn) {
@@ -319,11 +320,14 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
                 for (int u = 0; u < KC; u++) {
                     const int32_t *Sp = S + (jj + PFD * KC + u) * GT;
                     if (jj + PFD * KC + u < jn) {
-                        const int4 a = *reinterpret_cast<const int4 *>(Sp);
-                        const int4 b = *reinterpret_cast<const int4 *>(Sp + 4);
-                        const int32_t w[RPL] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                        int32_t w[RP];
 #pragma unroll
-                        for (int t = 0; t < RPL; t++)
+                        for (int h = 0; h < RP / 4; h++) {
+                            const int4 a = *reinterpret_cast<const int4 *>(Sp + 4 * h);
+                            w[4 * h] = a.x; w[4 * h + 1] = a.y; w[4 * h + 2] = a.z; w[4 * h + 3] = a.w;
+                        }
+#pragma unroll
+                        for (int t = 0; t < RP; t++)
                             if (t == 0 || w[t] != w[t - 1])
                                 asm volatile("prefetch.global.L1 [%0];" ::"l"(Fb + (size_t)(unsigned)w[t] * rowbytes));
                     }
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
 #pragma unroll
                 for (int i = 0; i < 4; i++) v[u][i] = 0;   // also the value of an absent chain
 #pragma unroll
-            for (int t = 0; t < RPL; t++) {
+            for (int t = 0; t < RP; t++) {
 #pragma unroll
                 for (int u = 0; u < KC; u++)
                     ld4_if_ne_pi(v[u], Fb + (size_t)(unsigned)id[u][t] * rowbytes, id[u][t],
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
         if (c == nchunk - 1) {
             const int64_t tile = it / G32;
 #pragma unroll
-            for (int t = 0; t < RPL; t++) {
+            for (int t = 0; t < RP; t++) {
                 const int32_t usr = out_user[tile * GT + pos0 + t];
                 if (usr >= 0) {
                     u64 o[4];
@@ -373,17 +377,17 @@ __global__ void __launch_bounds__(256, MINB) k_gather_pi(const int32_t *__restri
 static int g_pi_cfg = 0;
 void set_gather_pi_cfg(int c) { g_pi_cfg = c; }
 
-template <typename T, int KC, int MINB, bool STEP_IDS, int PFD>
+template <typename T, int KC, int MINB, bool STEP_IDS, int PFD, int RP = RPL>
 static cudaError_t gather_pi_t(const GatherPi &G, int32_t k, const void *F, void *g, int64_t B, int num_sms,
                                int contig, bool prefetch, cudaStream_t s) {
     const int G32 = (int)(B / 32);
     const int64_t items = (G.npad / GT) * G32;
     const size_t smem = (size_t)2 * KCH * GT * 4;
     const int64_t grid = std::min<int64_t>(items, (int64_t)num_sms * MINB);
-    auto kern = k_gather_pi<T, KC, MINB, STEP_IDS, PFD>;
+    auto kern = k_gather_pi<T, KC, MINB, STEP_IDS, PFD, RP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, 256, smem, s>>>(G.Mg, G.npad, k, (const T *)F, (T *)g, G.out_user, (int32_t)B,
+    kern<<<(unsigned)grid, 32 * GT / (4 * RP), smem, s>>>(G.Mg, G.npad, k, (const T *)F, (T *)g, G.out_user, (int32_t)B,
                                            G32, items, contig, prefetch ? (const int2 *)G.Fr : nullptr);
     launches_add(1);
     return cudaGetLastError();
@@ -405,6 +409,9 @@ static cudaError_t gather_pi_cfg(const GatherPi &G, int32_t k, const void *F, vo
         case 1: return gather_pi_t<T, 2, 2, false, 2>(G, k, F, g, B, num_sms, 1, true, s);
         case 2: return gather_pi_t<T, 2, 2, false, 0>(G, k, F, g, B, num_sms, 0, false, s);
         case 3: return gather_pi_t<T, 4, 2, true, 0>(G, k, F, g, B, num_sms, 0, false, s);
+        case 5: return gather_pi_t<T, 2, 2, false, 2, 4>(G, k, F, g, B, num_sms, 0, false, s);   // 4 positions per lane
+        case 6: return gather_pi_t<T, 2, 4, false, 2, 16>(G, k, F, g, B, num_sms, 0, false, s);  // 16 per lane
+        case 7: return gather_pi_t<T, 2, 1, false, 2, 4>(G, k, F, g, B, num_sms, 0, false, s);   // 4 per lane, 128 regs
         default: return gather_pi_t<T, 2, 2, false, 2>(G, k, F, g, B, num_sms, 0, false, s);
     }
 }

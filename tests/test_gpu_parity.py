@@ -328,7 +328,7 @@ def test_dense_gather_variants(variant):
         P.set_option("gather_variant", 0)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_gather_order_configs(cfg):
     """The gather-order kernel's configurations (option gather_pi_cfg; 4 is
     the delta-list gather) against O2, bit-exact int64 and fp64 within the
