@@ -551,3 +551,62 @@ def test_sparse_direct_rows_vs_dense_and_O2(inst, built):
     assert_fp64_close(gpu_zeta(Ps, ff), O.zeta(ff), O.zeta(np.abs(ff)))
     with pytest.raises(pz.PosetError):
         gpu_moebius(Ps, f, pz.MOEB_RINGDF)        # schedules that need the dense table refuse
+
+
+# ------------------------------------------- randomized schedule stress --
+# No race checker runs on this pool, so the hand-rolled
+# memory-ordering protocols of the ring schedules (mbarrier level phases,
+# DSMEM st.async with transaction counts, RINGCW's tagged records, the CSR
+# grid barrier) are exercised on many seeded random shapes: window DAGs of
+# random window / degree / size (levels of 1 to > 96 elements, reach from a
+# few ranks to the ring limit), layered DAGs of random width, each against O2
+# bit-exact in Z/2^64 under every schedule that applies.
+
+def _random_shapes():
+    rng = np.random.default_rng(2026)
+    for i in range(40):
+        kind = rng.integers(0, 3)
+        if kind < 2:
+            n = int(rng.integers(300, 12000))
+            Wd = int(rng.integers(3, 400))
+            d = int(rng.integers(1, 5))
+            yield f"win{i}_n{n}_W{Wd}_d{d}", n, *W.window_dag(n, d, Wd, int(rng.integers(0, 1000)),
+                                                              forced=bool(kind))
+        else:
+            L, w = int(rng.integers(8, 80)), int(rng.integers(4, 120))
+            yield f"lay{i}_{L}x{w}", L * w, *W.layered_dag(L, w, int(rng.integers(1, 4)), int(rng.integers(0, 1000)),
+                                                            forced=True)
+
+
+_SEEN = set()
+
+
+@pytest.mark.parametrize("shape", list(_random_shapes()), ids=lambda t: t[0])
+def test_schedules_on_random_shapes(shape):
+    name, n, src, dst = shape
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    _SEEN.update(kernels_for(P))
+    rng = np.random.default_rng(n)
+    for B in (1, int(rng.integers(2, 40))):
+        h = W.int_values(n, B, -10**17, 10**17, seed=B + 7)
+        want = O.moebius(h)
+        hd = dev(h)
+        for kern in [None] + kernels_for(P):
+            if kern in (pz.MOEB_LEVEL, pz.MOEB_GRID, pz.MOEB_WARP) and P.info()["ell"] > 2000:
+                continue
+            helpers = (1, 2, 3) if kern in (pz.MOEB_RINGCL, pz.MOEB_RINGCW) else (0,)
+            for nh in helpers:
+                P.set_option("ringcl_helpers", nh)
+                got = gpu_moebius_dev(P, hd, kern)
+                assert (got == want).all(), (name, B, kern, nh)
+        P.set_option("ringcl_helpers", 0)
+        f = W.int_values(n, B, -10**17, 10**17, seed=B + 8)
+        assert (gpu_zeta(P, f) == O.zeta(f)).all(), (name, B)
+
+
+def test_random_shapes_reached_the_ring_schedules():
+    """The stress set above is not vacuous: it ran RINGDF, RINGCL and RINGCW
+    and the sparse-row schedule on some shapes."""
+    if not _SEEN:
+        pytest.skip("run together with test_schedules_on_random_shapes")
+    assert {pz.MOEB_RINGDF, pz.MOEB_RINGCL, pz.MOEB_RINGCW, pz.MOEB_CSR} <= _SEEN, _SEEN
