@@ -272,7 +272,11 @@ poset_status poset_query(poset_t h, poset_info *out);
  * per-lane row reuse (default), 1..3 = its alternatives measured in
  * DESIGN.md §5.2, 4 = the delta-list gather: g carried from one gather
  * position to the next, only the changed chains' rows loaded, with an fp64
- * error certificate; its list is built on first use -- measured slower);
+ * error certificate; its list is built on first use -- measured slower;
+ * 5..7 = 4 / 16 / 4 positions per lane, measured slower);
+ * "ringcl_helpers" (RINGCL / RINGCW helper CTAs per column 1..3, 0 = auto);
+ * "ringcl_chunk" (RINGCL owner stage chunk 32..256 ranks, 0 = the plan's; tuning);
+ * "ringcw_sleep" (RINGCW level warps: ns between level polls, 0 = try_wait; tuning);
  * "compute_depth_u" (1: compute D_U now, synchronously, into poset_info.depth_u);
  * "profile" (0/1): record a CUDA event pair on the call's stream around every
  * kernel phase of subsequent calls (see poset_profile_read);
