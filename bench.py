@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--ringcl-helpers", type=int, default=0, help="RINGCL helper CTAs (tuning; 0 = auto)")
     ap.add_argument("--ringcw-sleep", type=int, default=-1, help="RINGCW level-warp poll interval ns (tuning)")
     ap.add_argument("--ringcl-chunk", type=int, default=0, help="RINGCL owner stage chunk (tuning; 0 = plan)")
+    ap.add_argument("--scan-mode", type=int, default=0, help="zeta scan: 0 auto, 1 single pass, 2 three kernels")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -277,6 +278,8 @@ def main():
         P.set_option("ring_debug", args.ring_debug)
     if args.ringcl_helpers:
         P.set_option("ringcl_helpers", args.ringcl_helpers)
+    if args.scan_mode:
+        P.set_option("scan_mode", args.scan_mode)
     if args.ringcl_chunk:
         P.set_option("ringcl_chunk", args.ringcl_chunk)
     if args.ringcw_sleep >= 0:

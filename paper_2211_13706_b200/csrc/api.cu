@@ -513,6 +513,8 @@ struct PhaseTimer {
 
 typedef poset_status (*device_fn)(poset_s *, const void *, void *, int64_t, int, cudaStream_t);
 
+static int g_scan_mode = 0;   // option scan_mode (process-wide, tuning): 0 auto, 1 single pass, 2 three kernels
+
 static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int dt, cudaStream_t s) {
     if (h->sharded)
         return fail(POSET_EINVAL, "poset_zeta: the index rows are sharded (poset_shard_rows); use the split phases");
@@ -568,7 +570,7 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
     h->info.gather_resets = h->gpi.nreset;
     {
         PhaseTimer t(h, POSET_PH_SCAN, s);
-        if (B <= 4)   // single pass (decoupled look-back); measured slower than the three-kernel scan for B = 32, 64
+        if (g_scan_mode == 1 || (g_scan_mode == 0 && B <= 4))   // single pass (decoupled look-back)
             CK(launch_scan_1p(P, dt, f, h->d_F, B, h->d_scan, s));
         else
             CK(launch_scan(P, dt, f, h->d_F, 0, h->H.n, B, h->d_scan, nullptr, s));
@@ -943,6 +945,11 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
                 return fail(POSET_EINVAL, "ringws_lpeo must leave 8 or 16 far entries per lane");
             h->rws.lpeo = (int32_t)value;
         }
+        return POSET_OK;
+    }
+    if (!strcmp(key, "scan_mode")) {   // process-wide zeta scan choice (tuning)
+        if (value < 0 || value > 2) return fail(POSET_EINVAL, "scan_mode is 0..2");
+        g_scan_mode = (int)value;
         return POSET_OK;
     }
     if (!strcmp(key, "ringcl_chunk")) {   // RINGCL owner stage chunk, ranks (tuning; 0 = the plan's)

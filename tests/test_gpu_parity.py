@@ -610,3 +610,23 @@ def test_random_shapes_reached_the_ring_schedules():
     if not _SEEN:
         pytest.skip("run together with test_schedules_on_random_shapes")
     assert {pz.MOEB_RINGDF, pz.MOEB_RINGCL, pz.MOEB_RINGCW, pz.MOEB_CSR} <= _SEEN, _SEEN
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_scan_modes(mode):
+    """Both zeta scans (single pass with a decoupled look-back, and
+    the three-kernel scan) against O2 over batch sizes that cover 1..32
+    columns per tile, several column groups and many tiles (long chains cross
+    hundreds of tiles), int64 bit-exact and fp64 within the tolerance."""
+    n = 60013
+    src, dst = W.window_dag(n, 2, 64, 11, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    P.set_option("scan_mode", mode)
+    try:
+        for B in (1, 3, 32, 33, 64, 96):
+            f = W.int_values(n, B, -10**15, 10**15, seed=B + 30)
+            assert (gpu_zeta(P, f) == O.zeta(f)).all(), B
+        ff = W.normal_values(n, 32, seed=5)
+        assert_fp64_close(gpu_zeta(P, ff), O.zeta(ff), O.zeta(np.abs(ff)))
+    finally:
+        P.set_option("scan_mode", 0)
