@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--ringcl-chunk", type=int, default=0, help="RINGCL owner stage chunk (tuning; 0 = plan)")
     ap.add_argument("--scan-mode", type=int, default=0, help="zeta scan: 0 auto, 1 single pass, 2 three kernels")
     ap.add_argument("--ring-debug", type=int, default=0, help="timing experiments only (invalid results)")
+    ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
+                    help="batched pipeline: batch i+1's zeta on the SMs batch i's ring-family Möbius "
+                         "leaves free (two streams; auto = when the Möbius leaves SMs free)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
@@ -323,8 +326,55 @@ def main():
             P.zeta(x, out=g)
             P.moebius(g, out=y)
 
-    for _ in range(args.warmup):
-        step()
+    # Batched pipeline: a ring-family Möbius occupies one
+    # cluster of SMs per column (C5w: 32 x 3 = 96 of 148) for ~100 ms, so
+    # batch i+1's zeta runs on the SMs it leaves free, on a second stream
+    # (the library orders only calls that share scratch: zeta and ring-family
+    # Möbius use disjoint lanes, include/poset.h).  The Möbius stream has the
+    # higher priority so its clusters are placed before the zeta's CTAs; the
+    # zeta's persistent gather grid is sized to the free SMs (option zeta_sms).
+    step()   # first call: builds the lazy tables and resolves the Möbius footprint
+    torch.cuda.synchronize()
+    inf0 = P.info()
+    ring_fam = MOEB_NAMES[inf0["moebius_kernel"]] in ("ring", "ringws", "ringdf", "ringcl", "ringcw")
+    free_sms = inf0["num_sms"] - inf0["moebius_sms"]
+    use_pipe = (not row_mode and B > 0 and ring_fam and free_sms >= 8 and args.pipeline != "off") or \
+        (args.pipeline == "on" and not row_mode and B > 0)
+    zeta_budget = max(free_sms, 1) if use_pipe else 0
+    if use_pipe:
+        s_z = torch.cuda.Stream(priority=0)
+        s_m = torch.cuda.Stream(priority=-1)
+        gb = [g, torch.empty_like(x)]
+        ev_z = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_m = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def run_steps(nsteps):
+        if not use_pipe:
+            for _ in range(nsteps):
+                step()
+            return
+        cur = torch.cuda.current_stream()
+        s_z.wait_stream(cur)
+        s_m.wait_stream(cur)
+        P.set_option("zeta_sms", 0)            # the prologue zeta has the whole GPU
+        P.zeta(x, out=gb[0], stream=s_z)
+        ev_z[0].record(s_z)
+        P.set_option("zeta_sms", zeta_budget)
+        for i in range(nsteps):
+            b = i % 2
+            s_m.wait_event(ev_z[b])
+            P.moebius(gb[b], out=y, stream=s_m)
+            ev_m[b].record(s_m)
+            if i + 1 < nsteps:
+                if i >= 1:                      # gb[1-b] was Möbius(i-1)'s input
+                    s_z.wait_event(ev_m[1 - b])
+                P.zeta(x, out=gb[1 - b], stream=s_z)
+                ev_z[1 - b].record(s_z)
+        cur.wait_stream(s_m)
+        cur.wait_stream(s_z)
+        P.set_option("zeta_sms", 0)
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     # correctness spot check of the timed computation (round trip)
     if wl.dtype == "i64":
@@ -340,8 +390,7 @@ def main():
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        step()
+    run_steps(args.steps)
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -387,9 +436,40 @@ def main():
             "frac": sb / (dom_ms / 1e3) / 1e9 / peak,
             "kernel_bytes": kernels[dom]["alg_bytes"], "kernel_frac": kernels[dom]["frac"],
             "traffic": traffic, "traffic_source": tsrc}
-    # the zeta gather is the kernel the north star's roofline target names
+    # the zeta gather is the kernel the north star's roofline target names;
+    # in the pipeline it runs on the SMs the Möbius leaves free, so its
+    # full-GPU rate comes from a serial pass after the timed region
+    serial_k = None
+    if use_pipe:
+        P.set_option("profile", 1)
+        P.profile_read()
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        sprof, _ = P.profile_read()
+        P.set_option("profile", 0)
+        serial_k = {}
+        for ph in ("scan", "gather", "perm", "moebius_solve"):
+            tms, calls = sprof[ph]
+            if calls:
+                per = tms / calls
+                serial_k[ph] = {"ms_per_call": per, "achieved_gbs": ab[ph] / (per / 1e3) / 1e9,
+                                "frac": ab[ph] / (per / 1e3) / 1e9 / peak}
+        for ph in kernels:
+            if ph in serial_k:
+                kernels[ph]["serial_ms_per_call"] = serial_k[ph]["ms_per_call"]
     zroof = None
-    if "gather" in kernels:
+    if serial_k and "gather" in serial_k:
+        zt, zsrc = ncu_traffic(args.config, "gather")
+        zroof = {"bound": "hbm", "kernel": kernels["gather"]["kernel"],
+                 "alg_bytes": kernels["gather"]["alg_bytes"],
+                 "alg_bytes_basis": "SURVEY §8(d) zeta bytes minus the scan's 16nB: 4nk + 16nB",
+                 "achieved": serial_k["gather"]["achieved_gbs"], "peak": peak, "peak_kind": peak_kind,
+                 "unit": "GB/s", "frac": serial_k["gather"]["frac"], "traffic": zt, "traffic_source": zsrc,
+                 "measured": "serial pass on all SMs after the timed region (in the pipeline the gather "
+                             f"runs on the {zeta_budget} SMs the Möbius leaves free: "
+                             f"{kernels['gather']['ms_per_call']:.2f} ms per call, overlapped)"}
+    elif "gather" in kernels:
         zt, zsrc = ncu_traffic(args.config, "gather")
         zroof = {"bound": "hbm", "kernel": kernels["gather"]["kernel"],
                  "alg_bytes": kernels["gather"]["alg_bytes"],
@@ -428,15 +508,19 @@ def main():
         # stays on the device)
         K = args.e2e_steps
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        # pipelined: the Möbius on its own high-priority stream (see run_steps)
+        s_mb = torch.cuda.Stream(priority=-1) if use_pipe else s_cmp
         xin = [torch.empty_like(x) for _ in range(2)]
         yout = [torch.empty_like(x) for _ in range(2)]
-        gd = torch.empty_like(x)
+        gd2 = [torch.empty_like(x) for _ in range(2)] if use_pipe else [torch.empty_like(x)] * 2
         res = [torch.empty_like(fp).pin_memory() for _ in range(2)]
         ev = lambda: torch.cuda.Event()
         in_done, in_free, out_done, out_free = [ev() for _ in range(2)], [ev() for _ in range(2)], \
             [ev() for _ in range(2)], [ev() for _ in range(2)]
+        z_done, g_free = [ev() for _ in range(2)], [ev() for _ in range(2)]
 
         def pipelined(steps):
+            P.set_option("zeta_sms", zeta_budget)
             for i in range(steps):
                 sl = i % 2
                 with torch.cuda.stream(s_in):
@@ -445,16 +529,22 @@ def main():
                     xin[sl].copy_(fp, non_blocking=True)
                     in_done[sl].record(s_in)
                 s_cmp.wait_event(in_done[sl])
-                if i >= 2:
-                    s_cmp.wait_event(out_free[sl])
-                P.zeta(xin[sl], out=gd, stream=s_cmp)
+                if i >= 2 and use_pipe:
+                    s_cmp.wait_event(g_free[sl])
+                P.zeta(xin[sl], out=gd2[sl], stream=s_cmp)
                 in_free[sl].record(s_cmp)
-                P.moebius(gd, out=yout[sl], stream=s_cmp)
-                out_done[sl].record(s_cmp)
+                z_done[sl].record(s_cmp)
+                s_mb.wait_event(z_done[sl])
+                if i >= 2:
+                    s_mb.wait_event(out_free[sl])
+                P.moebius(gd2[sl], out=yout[sl], stream=s_mb)
+                g_free[sl].record(s_mb)
+                out_done[sl].record(s_mb)
                 with torch.cuda.stream(s_out):
                     s_out.wait_event(out_done[sl])
                     res[sl].copy_(yout[sl], non_blocking=True)
                     out_free[sl].record(s_out)
+            P.set_option("zeta_sms", 0)
 
         pipelined(2)
         torch.cuda.synchronize()
@@ -463,9 +553,11 @@ def main():
         if world > 1:
             torch.distributed.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_in.wait_stream(torch.cuda.current_stream())
         a0.record(s_in)
         pipelined(K)
         s_in.wait_stream(s_out)
+        s_in.wait_stream(s_mb)
         a1.record(s_in)
         torch.cuda.synchronize()
         ems = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
@@ -476,10 +568,13 @@ def main():
                "h2d_bytes_per_step": n * GB * 8, "d2h_bytes_per_step": n * GB * 8,
                "ms_per_step": ems / K, "steps": K,
                "round_trip_exact": rt_ok if wl.dtype == "i64" else None,
-               "path": ("per step: f (pinned host) -> device copy, poset_zeta + poset_moebius on one "
-                        "compute stream (g stays on the device), result -> pinned host copy; copies on "
-                        "their own streams, overlapping the neighbouring steps' transforms")}
-        del xin, yout, gd, res
+               "path": ("per step: f (pinned host) -> device copy, poset_zeta then poset_moebius (g stays "
+                        "on the device" + ("; the Möbius on its own high-priority stream, so batch i+1's "
+                                           "zeta overlaps batch i's Möbius" if use_pipe else
+                                           ", one compute stream") +
+                        "), result -> pinned host copy; copies on their own streams, overlapping the "
+                        "neighbouring steps' transforms")}
+        del xin, yout, gd2, res
         # (b) context: both transforms staged through host memory by the library
         # itself (zeta host -> host, Möbius host -> host, serial)
         gp = torch.empty_like(fp).pin_memory()
@@ -532,6 +627,12 @@ def main():
                        "parallelism": (f"zeta row-shard x{world} + NCCL all-gather, Möbius on rank 0"
                                        if row_mode else f"column-shard x{world}"),
                        "depth_u": P.info()["depth_u"], "provenance": prov, "index_shard": shard,
+                       "pipeline": ({"zeta_sms": zeta_budget, "moebius_sms": inf0["moebius_sms"],
+                                     "how": "batch i+1's zeta (low-priority stream, gather grid on the free "
+                                            "SMs) overlaps batch i's Möbius (high-priority stream); every "
+                                            "step still runs scan, gather, permutation and U-solve on its "
+                                            "own batch"}
+                                    if use_pipe else None),
                        "l2": "inputs > L2 (index table 4nk B, F 8nB B): no flush needed"},
             "gbs_per_step": sum(ab[p] for p in kernels) / (ms_max / args.steps / 1e3) / 1e9,
             # nnz(N)·B per second: the work the method needs;

@@ -28,10 +28,18 @@
  *             default stream).  Compute calls are asynchronous and
  *             stream-ordered; setup is synchronous.
  *  Threads    a handle is not re-entrant: serialise calls per handle (host
- *             side).  Calls on DIFFERENT streams are ordered by the library:
- *             each call records an event on its stream and a call on another
- *             stream waits on it first, because all calls share the handle's
- *             scratch buffers.  A host result is valid once `stream` has
+ *             side).  Calls on DIFFERENT streams are ordered by the library
+ *             wherever they share handle scratch: the scratch is split in
+ *             three lanes (Z: the zeta's scan / gather buffers and the
+ *             non-ring Möbius schedules; R: the ring-family Möbius input;
+ *             S: host staging); each call records an event per lane it uses
+ *             on its stream, and a call on another stream first waits on the
+ *             events of its own lanes.  So a zeta on one stream and a
+ *             ring-family Möbius (poset_info.moebius_kernel RING / RINGWS /
+ *             RINGDF / RINGCL / RINGCW) on another, both on device buffers,
+ *             run concurrently; everything else is serialised.  Data
+ *             dependencies between the caller's own buffers are the caller's
+ *             to order (events).  A host result is valid once `stream` has
  *             synchronised (poset_sync).
  *  Errors     return codes, never exceptions; poset_last_error() gives the
  *             calling thread's last message.  CUDA faults inside a kernel
@@ -86,7 +94,7 @@ typedef enum {
     POSET_MOEB_RING = 4,      /* bounded-reach posets: one CTA per column, F in a shared-memory
                                  ring, U-solve and chain difference fused   */
     POSET_MOEB_CSR = 5,       /* sparse U-rows, persistent kernel with a grid barrier per
-                                 level, one warp per (element, column group) (DESIGN.md §5.5) */
+                                 level, one warp per (element, column group) (DESIGN.md §5.3) */
     POSET_MOEB_RINGWS = 6,    /* RING with warp specialisation: one warp on the level-by-level
                                  critical path (near dependencies only), the others summing the
                                  far dependencies ahead of it                 */
@@ -140,6 +148,9 @@ typedef struct {
     int64_t gather_entries; /* entries of the zeta delta list (changed niv slots
                              between consecutive gather positions) */
     int64_t gather_resets;  /* positions summed from scratch in that list         */
+    int64_t moebius_sms;  /* SMs the last poset_moebius launch occupied (ring family:
+                             one CTA per SM; 0 = no call yet)                        */
+    int64_t num_sms;      /* SMs of the handle's device                              */
 } poset_info;
 
 /*
@@ -274,6 +285,10 @@ poset_status poset_query(poset_t h, poset_info *out);
  * position to the next, only the changed chains' rows loaded, with an fp64
  * error certificate; its list is built on first use -- measured slower;
  * 5..7 = 4 / 16 / 4 positions per lane, measured slower);
+ * "zeta_sms" (0 = all SMs): the SM count the zeta's persistent gather grids
+ * size for -- set it to the SMs a concurrent ring-family Möbius on another
+ * stream leaves free (num_sms - poset_info.moebius_sms), so the gather does
+ * not queue CTAs behind the Möbius (the batched pipeline);
  * "ringcl_helpers" (RINGCL / RINGCW helper CTAs per column 1..3, 0 = auto);
  * "ringcl_chunk" (RINGCL owner stage chunk 32..256 ranks, 0 = the plan's; tuning);
  * "ringcw_sleep" (RINGCW level warps: ns between level polls, 0 = try_wait; tuning);

@@ -54,7 +54,8 @@ class PosetInfo(ctypes.Structure):
                 ("csr_bytes", _i64), ("zeta_sparse", _i64), ("ringws", _i64), ("ringdf", _i64),
                 ("rdf_bytes", _i64), ("ring_bytes", _i64), ("rws_bytes", _i64),
                 ("depth_u", _i64), ("t_depth", ctypes.c_double), ("gather_bytes", _i64),
-                ("gather_entries", _i64), ("gather_resets", _i64)]
+                ("gather_entries", _i64), ("gather_resets", _i64),
+                ("moebius_sms", _i64), ("num_sms", _i64)]
 
 
 def _sig(name, args, res=ctypes.c_int):
@@ -87,6 +88,10 @@ _sig("poset_last_error", [], ctypes.c_char_p)
 _sig("poset_shard_rows", [_vp, _i64, _i64, ctypes.c_uint32])
 _sig("poset_abi_version", [], ctypes.c_int)
 _sig("poset_sync", [_vp, _vp])
+ABI_VERSION = 2   # poset_info layout (PosetInfo) this binding marshals
+if lib.poset_abi_version() != ABI_VERSION:
+    raise ImportError(f"libposet.so ABI {lib.poset_abi_version()} != binding ABI {ABI_VERSION}: rebuild "
+                      "(python -c 'import __graft_entry__ as g; g.build()')")
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "ESELFLOOP", 3: "ECYCLE", 4: "ENOTCHAIN", 5: "ENOTPARTITION",
           6: "ETOOBIG", 7: "ENOMEM", 8: "ECUDA"}

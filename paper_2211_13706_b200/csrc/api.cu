@@ -31,13 +31,17 @@ struct poset_s {
     poset_info info{};
     int moeb_opt = MOEB_AUTO;
     cudaError_t sticky = cudaSuccess;
-    // cross-stream ordering of calls on one handle: every call records
-    // done_ev on its stream; a call on a different stream first waits on it,
-    // so the handle's scratch (F, scan, partial, staging) is never shared by
-    // two calls in flight
-    cudaEvent_t done_ev = nullptr;
-    cudaStream_t last_s = nullptr;
-    bool used = false;
+    // cross-stream ordering of calls on one handle, per scratch lane: a call
+    // records lane_ev[l] on its stream for every lane l it uses, and a call on
+    // a different stream first waits on those lanes' events -- so no scratch
+    // buffer is shared by two calls in flight, while a zeta (lane Z) and a
+    // ring-family Möbius (lane R) on two streams may run concurrently
+    //   lane Z: d_F, d_scan, d_part, d_bar, the lazily built gather order;
+    //   lane R: d_gP (rank-major g of the ring schedules);  lane S: d_stage
+    cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t lane_s[3] = {nullptr, nullptr, nullptr};
+    bool lane_used[3] = {false, false, false};
+    int zeta_sms = 0;                 // option zeta_sms: SMs the zeta's persistent grids size for
     // device residency
     int32_t *d_rank_user = nullptr, *d_slot = nullptr, *d_chain = nullptr, *d_lvl = nullptr;
     int32_t *d_child = nullptr, *d_slot_user = nullptr, *d_M = nullptr;
@@ -129,7 +133,8 @@ static void free_all(poset_s *h) {
     cudaSetDevice(h->device);
     for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
-    if (h->done_ev) cudaEventDestroy(h->done_ev);
+    for (auto e : h->lane_ev)
+        if (e) cudaEventDestroy(e);
     free_gather_pi(h->gpi);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
@@ -162,7 +167,7 @@ static poset_status finish_setup_sparse(poset_s *h, double t0, size_t table, siz
     CK(upload(&h->d_child_ptr, H.child_ptr));
     CK(upload(&h->d_child, H.child));
     CK(upload(&h->d_slot_user, H.slot_user));
-    CK(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
+    for (auto &e : h->lane_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMalloc((void **)&h->d_bar, 64));
     CK(cudaMalloc((void **)&h->d_count, 64));
     int32_t *d_slot_chain = nullptr, *d_chain_off = nullptr;
@@ -240,7 +245,7 @@ static poset_status finish_setup(poset_s *h) {
     CK(upload(&h->d_child_ptr, H.child_ptr));
     CK(upload(&h->d_child, H.child));
     CK(upload(&h->d_slot_user, H.slot_user));
-    CK(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
+    for (auto &e : h->lane_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMalloc((void **)&h->d_bar, 64));
     CK(cudaMalloc((void **)&h->d_count, 64));
     CK(cudaMalloc((void **)&h->d_M, std::max<size_t>(table, 4)));
@@ -464,16 +469,23 @@ static bool is_device_ptr(const void *p) {
 // vector loads and stores need (the transforms stage anything else).
 static bool dev_aligned(const void *p) { return is_device_ptr(p) && ((uintptr_t)p % 32) == 0; }
 
-static poset_status begin_call(poset_s *h, cudaStream_t s) {
-    if (h->used && s != h->last_s) CK(cudaStreamWaitEvent(s, h->done_ev, 0));
+enum : unsigned { LANE_Z = 1, LANE_R = 2, LANE_S = 4, LANE_ALL = 7 };
+
+static poset_status begin_call(poset_s *h, cudaStream_t s, unsigned lanes = LANE_ALL) {
+    for (int l = 0; l < 3; l++)
+        if ((lanes >> l & 1) && h->lane_used[l] && s != h->lane_s[l])
+            CK(cudaStreamWaitEvent(s, h->lane_ev[l], 0));
     return POSET_OK;
 }
 
-static poset_status end_call(poset_s *h, cudaStream_t s, poset_status st) {
+static poset_status end_call(poset_s *h, cudaStream_t s, poset_status st, unsigned lanes = LANE_ALL) {
     if (st != POSET_OK) return st;
-    CK(cudaEventRecord(h->done_ev, s));
-    h->last_s = s;
-    h->used = true;
+    for (int l = 0; l < 3; l++)
+        if (lanes >> l & 1) {
+            CK(cudaEventRecord(h->lane_ev[l], s));
+            h->lane_s[l] = s;
+            h->lane_used[l] = true;
+        }
     return POSET_OK;
 }
 
@@ -522,7 +534,10 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
     if (st) return st;
     st = grow(h, &h->d_scan, &h->scan_bytes, std::max(scan_scratch_bytes(h->H.n, B), scan1p_scratch_bytes(h->H.n, B)));
     if (st) return st;
-    size_t pb = gather_partial_bytes(h->dev(), h->H.n, B, h->num_sms);
+    // persistent gather grids size for the zeta's SM budget (option zeta_sms:
+    // the SMs a concurrent Möbius on another stream leaves free)
+    const int zs = h->zeta_sms > 0 ? std::min(h->zeta_sms, h->num_sms) : h->num_sms;
+    size_t pb = gather_partial_bytes(h->dev(), h->H.n, B, zs);
     if (pb) {
         st = grow(h, &h->d_part, &h->part_bytes, pb);
         if (st) return st;
@@ -580,27 +595,37 @@ static poset_status zeta_dev(poset_s *h, const void *f, void *g, int64_t B, int 
         if (h->zeta_csr)
             CK(launch_gather_csr(P, h->csr, dt, h->d_F, g, 0, h->H.n, B, 0, s));
         else if (use_delta)
-            CK(launch_gather_delta(h->gpi, h->H.n, h->H.k, dt, h->d_F, g, B, h->num_sms, s));
+            CK(launch_gather_delta(h->gpi, h->H.n, h->H.k, dt, h->d_F, g, B, zs, s));
         else if (use_pi)
-            CK(launch_gather_pi(h->gpi, h->H.k, dt, h->d_F, g, B, h->num_sms, s));
+            CK(launch_gather_pi(h->gpi, h->H.k, dt, h->d_F, g, B, zs, s));
         else
-            CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, h->num_sms, s));
+            CK(launch_gather(P, dt, h->d_F, g, 0, h->H.n, B, 0, pb ? h->d_part : nullptr, zs, s));
     }
     return POSET_OK;
 }
 
+// AUTO: the CTA-pair schedule when two SMs per column fit in one wave
+static int moebius_which(const poset_s *h, int64_t B) {
+    return h->moeb_opt != MOEB_AUTO ? h->moeb_opt
+           : (ringcl_fits(h->rdf) && 2 * B <= h->num_sms) ? MOEB_RINGCL
+           : h->rdf.ok  ? MOEB_RINGDF
+           : h->rws.ok  ? MOEB_RINGWS
+           : h->ring.ok ? MOEB_RING
+           : h->csr.ok  ? MOEB_CSR
+                        : moebius_pick(h->dev(), B, h->H.max_level_width, h->num_sms);
+}
+
+// the ring family reads only d_gP (lane R); the others use d_F / d_bar (lane Z)
+static bool ring_family(int which) {
+    return which == MOEB_RINGDF || which == MOEB_RINGCL || which == MOEB_RINGCW || which == MOEB_RINGWS ||
+           which == MOEB_RING;
+}
+
 static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, int dt, cudaStream_t s) {
-    poset_status st = ensure_F(h, B, s);
-    if (st) return st;
+    poset_status st = POSET_OK;
     DevPoset P = h->dev();
-    // AUTO: the CTA-pair schedule when two SMs per column fit in one wave
-    int which = h->moeb_opt != MOEB_AUTO ? h->moeb_opt
-                : (ringcl_fits(h->rdf) && 2 * B <= h->num_sms) ? MOEB_RINGCL
-                : h->rdf.ok  ? MOEB_RINGDF
-                : h->rws.ok  ? MOEB_RINGWS
-                : h->ring.ok ? MOEB_RING
-                : h->csr.ok  ? MOEB_CSR
-                             : moebius_pick(P, B, h->H.max_level_width, h->num_sms);
+    const int which = moebius_which(h, B);
+    if (!ring_family(which) && (st = ensure_F(h, B, s))) return st;
     if (h->sharded && (which == MOEB_LEVEL || which == MOEB_GRID || which == MOEB_WARP))
         return fail(POSET_EINVAL, "poset_moebius: the index rows are sharded (poset_shard_rows); the LEVEL / "
                                   "GRID / WARP schedules read the whole table");
@@ -612,10 +637,12 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
             return fail(POSET_EINVAL, "poset_moebius: the CSR schedule has no sparse rows for this "
                                       "poset (not built: RING applies or memory); use AUTO");
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
+        h->info.moebius_sms = h->num_sms;
         CK(launch_moebius_csr(P, h->csr, dt, g, h->d_F, f, B, h->d_bar, h->num_sms, s));
         return POSET_OK;
     }
     h->info.moebius_kernel = which;
+    h->info.moebius_sms = ring_family(which) ? std::min<int64_t>(B, h->num_sms) : h->num_sms;
     if (which == MOEB_RINGDF || which == MOEB_RINGCL || which == MOEB_RINGCW) {
         if (!h->rdf.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGDF schedule does not fit this poset; use AUTO");
@@ -632,7 +659,10 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
         if (which == MOEB_RINGCL || which == MOEB_RINGCW) {
             h->rdf.cw = which == MOEB_RINGCW;
-            cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s);
+            int ctas = 0;
+            cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s,
+                                                   &ctas);
+            if (ce == cudaSuccess) h->info.moebius_sms = std::min(ctas, h->num_sms);
             if (ce == cudaErrorInvalidConfiguration && h->moeb_opt == MOEB_AUTO) {   // no cluster fits: RINGDF
                 cudaGetLastError();
                 h->info.moebius_kernel = MOEB_RINGDF;
@@ -713,6 +743,10 @@ static poset_status run_staged(poset_s *h, device_fn fn, const void *in, void *o
     return POSET_OK;
 }
 
+static bool needs_staging(const void *in, const void *out) {
+    return !(is_device_ptr(in) && ((uintptr_t)in % 32) == 0) || !(is_device_ptr(out) && ((uintptr_t)out % 32) == 0);
+}
+
 extern "C" {
 
 poset_status poset_zeta(poset_t h, const void *f, void *g, int64_t batch, poset_dtype dt, void *stream) {
@@ -720,8 +754,9 @@ poset_status poset_zeta(poset_t h, const void *f, void *g, int64_t batch, poset_
     if (st || h->H.n == 0) return st;
     CK(cudaSetDevice(h->device));
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = begin_call(h, s))) return st;
-    return end_call(h, s, run_staged(h, zeta_dev, f, g, batch, dt, s));
+    const unsigned lanes = LANE_Z | (needs_staging(f, g) ? LANE_S : 0);
+    if ((st = begin_call(h, s, lanes))) return st;
+    return end_call(h, s, run_staged(h, zeta_dev, f, g, batch, dt, s), lanes);
 }
 
 poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, poset_dtype dt,
@@ -730,8 +765,10 @@ poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, pos
     if (st || h->H.n == 0) return st;
     CK(cudaSetDevice(h->device));
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = begin_call(h, s))) return st;
-    return end_call(h, s, run_staged(h, moebius_dev, g, f, batch, dt, s));
+    const unsigned lanes = (ring_family(moebius_which(h, batch)) ? LANE_R : LANE_Z) |
+                           (needs_staging(g, f) ? LANE_S : 0);
+    if ((st = begin_call(h, s, lanes))) return st;
+    return end_call(h, s, run_staged(h, moebius_dev, g, f, batch, dt, s), lanes);
 }
 
 // Split phases: caller pointers go straight to the kernels (no staging), so
@@ -916,6 +953,7 @@ poset_status poset_analyze(int64_t n, int64_t m, const int64_t *src, const int64
 poset_status poset_query(poset_t h, poset_info *out) {
     if (!h || !out) return fail(POSET_EINVAL, "poset_query: null argument");
     *out = h->info;
+    out->num_sms = h->num_sms;
     return POSET_OK;
 }
 
@@ -945,6 +983,11 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
                 return fail(POSET_EINVAL, "ringws_lpeo must leave 8 or 16 far entries per lane");
             h->rws.lpeo = (int32_t)value;
         }
+        return POSET_OK;
+    }
+    if (!strcmp(key, "zeta_sms")) {   // SMs the zeta's persistent grids size for (0 = all)
+        if (value < 0 || value > 4096) return fail(POSET_EINVAL, "poset_set_option: zeta_sms is 0..4096");
+        h->zeta_sms = (int)value;
         return POSET_OK;
     }
     if (!strcmp(key, "scan_mode")) {   // process-wide zeta scan choice (tuning)
@@ -1121,6 +1164,6 @@ const char *poset_strerror(poset_status s) {
 
 const char *poset_last_error(void) { return g_last_error.c_str(); }
 
-int poset_abi_version(void) { return 1; }
+int poset_abi_version(void) { return 2; }   // 2: poset_info.moebius_sms / num_sms
 
 }  // extern "C"

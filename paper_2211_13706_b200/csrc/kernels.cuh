@@ -211,7 +211,8 @@ bool ringcl_fits(const RingDFPlan &R);
 bool ringcw_fits(const RingDFPlan &R);
 void ringcl_plan(RingDFPlan &R);
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t batch, int num_sms, cudaStream_t s);
+                                  int dtype, const void *gP, void *f, int64_t batch, int num_sms, cudaStream_t s,
+                                  int *ctas_out = nullptr);   // CTAs (one per SM) of the launch
 
 // ---- sparse U-rows (moebius_csr.cu): zeta gather + Möbius over CSR rows ----
 struct CsrRows {

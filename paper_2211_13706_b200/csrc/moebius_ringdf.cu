@@ -1511,7 +1511,8 @@ bool ringcl_fits(const RingDFPlan &R) { return R.cl_ok; }
 bool ringcw_fits(const RingDFPlan &R) { return R.cw_ok; }
 
 cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const int32_t *ru_pad,
-                                  int dtype, const void *gP, void *f, int64_t B, int num_sms, cudaStream_t s) {
+                                  int dtype, const void *gP, void *f, int64_t B, int num_sms, cudaStream_t s,
+                                  int *ctas_out) {
     // two helper CTAs per column when three SMs per column fit one wave
     // (measured on C5w: 1 helper 128.0 ms, 2 helpers 100.4, 3 helpers 103.7;
     // three stay available through the ringcl_helpers option)
@@ -1531,7 +1532,7 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
         R2.nstage_h = R2.nstage;
         R2.ch_cl = 0;
         if (R2.nstage > kMaxStageCL || ringcl_smem_bytes(R2, R2.cw) > kSmemCapDF) return cudaErrorInvalidValue;
-        return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s);
+        return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s, ctas_out);
     }
     RDFArgs a{};
     a.Dn = R.D;
@@ -1610,11 +1611,12 @@ cudaError_t launch_moebius_ringcl(const DevPoset &P, const RingDFPlan &R, const 
         if (nh > 1 && !R.prof) {
             RingDFPlan R2 = R;
             R2.nh_force = nh - 1;
-            return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s);
+            return launch_moebius_ringcl(P, R2, ru_pad, dtype, gP, f, B, num_sms, s, ctas_out);
         }
         return cudaErrorInvalidConfiguration;
     }
     void *args[] = {&a};
+    if (ctas_out) *ctas_out = (int)(cdim * B);
     launches_add(1);
     return cudaLaunchKernelExC(&cfg, fn, args);
 }

@@ -37,7 +37,7 @@ def test_so_is_sm100a():
 
 
 def test_abi_version_and_strerror():
-    assert pz.lib.poset_abi_version() == 1
+    assert pz.lib.poset_abi_version() == 2
     assert pz.lib.poset_strerror(6) == b"dense table too big for device memory"
 
 

@@ -630,3 +630,56 @@ def test_scan_modes(mode):
         assert_fp64_close(gpu_zeta(P, ff), O.zeta(ff), O.zeta(np.abs(ff)))
     finally:
         P.set_option("scan_mode", 0)
+
+
+def test_pipelined_zeta_and_moebius_on_two_streams():
+    """The batched pipeline (bench --pipeline): zetas on one
+    stream, with the persistent gather grid sized to the SMs the Möbius leaves
+    free (option zeta_sms), overlapping ring-family Möbius calls on a second,
+    high-priority stream -- the two use disjoint scratch lanes
+    (include/poset.h), so the library does not serialise them.  Every batch:
+    zeta vs O2 bit-exact (int64) and the Möbius round trip exact; then two
+    zetas on two streams (same lane: ordered by the library) and a 3-SM zeta
+    budget, both vs O2."""
+    n = 120_000
+    src, dst = W.window_dag(n, 2, 64, 3, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    B = 32
+    fs = [W.int_values(n, B, -10**15, 10**15, seed=50 + i) for i in range(4)]
+    xs = [dev(f) for f in fs]
+    P.moebius(P.zeta(xs[0]))
+    torch.cuda.synchronize()
+    info = P.info()
+    assert info["moebius_kernel"] in (pz.MOEB_RINGCL, pz.MOEB_RINGDF)
+    assert 0 < info["moebius_sms"] < info["num_sms"]
+    P.set_option("zeta_sms", info["num_sms"] - info["moebius_sms"])
+    try:
+        cur = torch.cuda.current_stream()
+        s_z, s_m = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+        s_z.wait_stream(cur)
+        s_m.wait_stream(cur)
+        gs = [torch.empty_like(x) for x in xs]
+        ys = [torch.empty_like(x) for x in xs]
+        ev = [torch.cuda.Event() for _ in xs]
+        for i, x in enumerate(xs):        # zeta i+1.. queue behind zeta i, Möbius i overlaps them
+            P.zeta(x, out=gs[i], stream=s_z)
+            ev[i].record(s_z)
+            s_m.wait_event(ev[i])
+            P.moebius(gs[i], out=ys[i], stream=s_m)
+        torch.cuda.synchronize()
+        for i, f in enumerate(fs):
+            assert (host(gs[i]) == O.zeta(f)).all(), i
+            assert (host(ys[i]) == f).all(), i
+        a, b = torch.cuda.Stream(), torch.cuda.Stream()
+        a.wait_stream(cur)
+        b.wait_stream(cur)
+        g1, g2 = torch.empty_like(xs[1]), torch.empty_like(xs[2])
+        P.zeta(xs[1], out=g1, stream=a)
+        P.zeta(xs[2], out=g2, stream=b)
+        torch.cuda.synchronize()
+        assert (host(g1) == O.zeta(fs[1])).all()
+        assert (host(g2) == O.zeta(fs[2])).all()
+        P.set_option("zeta_sms", 3)
+        assert (gpu_zeta(P, fs[3]) == O.zeta(fs[3])).all()
+    finally:
+        P.set_option("zeta_sms", 0)
