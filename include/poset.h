@@ -335,6 +335,41 @@ poset_status poset_export_mtable(poset_t h, int32_t *out);
  * [3] next-level prefetch, [4] barrier, [5] levels). */
 poset_status poset_debug_read(poset_t h, int64_t *out8);
 
+/*
+ * NVLS multicast (the row-sharded zeta's all-gather of F
+ * fused into the scan epilogue, P:L738-745 row sharding).
+ *
+ * poset_nvls_create -- one buffer of `bytes` (rounded up to the multicast
+ *   granularity) on each of the ndev CUDA ordinals `devices` (this process
+ *   drives all of them), bound to one NVLS multicast object: a store through
+ *   the multicast address lands at the same offset of every device's buffer
+ *   (NVSwitch replicates it).  The library owns the memory; free it with
+ *   poset_nvls_destroy (which synchronises the device).  ECUDA when the
+ *   driver or the device has no multicast support (the caller falls back to
+ *   the NCCL all-gather path), ENOMEM when the memory does not fit.
+ *   (Sharing the object across processes -- one process per GPU -- needs a
+ *   shareable-handle exchange that is not built: the pool has one GPU.)
+ * poset_nvls_ptrs -- *mc: the multicast address (device-visible on every
+ *   listed device; only multimem.* instructions may use it); uc[i]: the
+ *   plain (unicast) address of device i's buffer; *bytes: the rounded size.
+ *
+ * poset_scan_slots_mc -- poset_scan_slots (Eq. zeta_cache P:L390-400 over
+ *   slots [lo, hi)), but every F row is stored with multimem.st through the
+ *   multicast address F_mc (F_mc + slot * batch * 8 is slot's row): all
+ *   devices bound to the object receive the rank's rows, so no separate
+ *   all-gather of F follows.  The kernel ends with a system-scope fence;
+ *   a peer may read the rows after its stream is ordered after this call's
+ *   completion (an event, or a collective that follows it on this stream).
+ *   tail: as poset_scan_slots.  F_mc: 8-byte aligned multicast address of
+ *   a buffer of >= n * batch * 8 bytes; f: 32-byte aligned device memory.
+ */
+typedef struct poset_nvls_s *poset_nvls_t;
+poset_status poset_nvls_create(const int *devices, int ndev, int64_t bytes, poset_nvls_t *out);
+poset_status poset_nvls_ptrs(poset_nvls_t b, void **mc, void **uc, int64_t *bytes);
+void poset_nvls_destroy(poset_nvls_t b);
+poset_status poset_scan_slots_mc(poset_t h, const void *f, void *F_mc, void *tail, int64_t slot_lo,
+                                 int64_t slot_hi, int64_t batch, poset_dtype dt, void *stream);
+
 /* poset_sync -- cudaStreamSynchronize(stream) on the handle's device (host
  * results of poset_zeta / poset_moebius are valid after it). */
 poset_status poset_sync(poset_t h, void *stream);

@@ -18,6 +18,7 @@ importing the binding raises ``ImportError`` (build it with
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -88,6 +89,10 @@ _sig("poset_last_error", [], ctypes.c_char_p)
 _sig("poset_shard_rows", [_vp, _i64, _i64, ctypes.c_uint32])
 _sig("poset_abi_version", [], ctypes.c_int)
 _sig("poset_sync", [_vp, _vp])
+_sig("poset_nvls_create", [ctypes.POINTER(ctypes.c_int), ctypes.c_int, _i64, ctypes.POINTER(_vp)])
+_sig("poset_nvls_ptrs", [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64)])
+_sig("poset_nvls_destroy", [_vp], None)
+_sig("poset_scan_slots_mc", [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp])
 ABI_VERSION = 2   # poset_info layout (PosetInfo) this binding marshals
 if lib.poset_abi_version() != ABI_VERSION:
     raise ImportError(f"libposet.so ABI {lib.poset_abi_version()} != binding ABI {ABI_VERSION}: rebuild "
@@ -287,6 +292,14 @@ class Poset:
         _check(lib.poset_scan_slots(self._h, _ptr(f), _ptr(F), _ptr(tail), lo, hi, B,
                                     _dtype_code(f), _stream_ptr(stream, f)))
 
+    def scan_slots_mc(self, f, F_mc: int, tail, lo, hi, stream=None):
+        """scan_slots with every F row stored through the NVLS multicast
+        address ``F_mc`` (an ``NvlsBuffer.mc``): the all-gather of F fused
+        into the scan epilogue (poset_scan_slots_mc)."""
+        B = f.shape[1] if f.ndim == 2 else 1
+        _check(lib.poset_scan_slots_mc(self._h, _ptr(f), _vp(int(F_mc)), _ptr(tail), lo, hi, B,
+                                       _dtype_code(f), _stream_ptr(stream, f)))
+
     def scan_carry(self, F, carry, lo, hi, stream=None):
         B = F.shape[1] if F.ndim == 2 else 1
         _check(lib.poset_scan_carry(self._h, _ptr(F), _ptr(carry), lo, hi, B, _dtype_code(F),
@@ -310,3 +323,50 @@ class Poset:
         B = g_rank.shape[1] if g_rank.ndim == 2 else 1
         _check(lib.poset_rank_to_user(self._h, _ptr(g_rank), _ptr(g_user), B,
                                       _dtype_code(g_rank), _stream_ptr(stream, g_rank)))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "strides": None, "version": 3}
+
+
+class NvlsBuffer:
+    """One buffer per listed device bound to an NVLS multicast object
+    (poset_nvls_create): a store through ``mc`` lands on every device's
+    buffer.  ``tensor(i, shape, dtype)`` views device i's buffer."""
+
+    def __init__(self, devices, nbytes: int):
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = _vp()
+        _check(lib.poset_nvls_create(devs, len(devices), int(nbytes), ctypes.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        mc = _vp()
+        uc = (_vp * len(devices))()
+        nb = _i64()
+        _check(lib.poset_nvls_ptrs(h, ctypes.byref(mc), uc, ctypes.byref(nb)))
+        self.mc = int(mc.value)
+        self.uc = [int(u) for u in uc]
+        self.nbytes = int(nb.value)
+
+    def tensor(self, i: int, shape, dtype):
+        torch = _torch()
+        item = torch.empty((), dtype=dtype).element_size()
+        if math.prod(shape) * item > self.nbytes:
+            raise ValueError("view larger than the buffer")
+        typestr = {torch.float64: "<f8", torch.int64: "<i8"}[dtype]
+        return torch.as_tensor(_CudaArray(self.uc[i], shape, typestr), device=f"cuda:{self.devices[i]}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.poset_nvls_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -2,6 +2,7 @@
 // point.  Host setup (setup.cpp) + device residency + kernel launches
 // (kernels.cu).  No compute step runs on the host: every transform step is a
 // CUDA kernel; without a GPU every compute call returns POSET_ECUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -787,6 +788,22 @@ static poset_status check_split(const char *fn, std::initializer_list<const void
     return POSET_OK;
 }
 
+poset_status poset_scan_slots_mc(poset_t h, const void *f, void *F_mc, void *tail, int64_t lo, int64_t hi,
+                                 int64_t batch, poset_dtype dt, void *stream) {
+    poset_status st = check_call(h, f, F_mc, batch, dt, "poset_scan_slots_mc");
+    if (st) return st;
+    if (lo < 0 || hi > h->H.n || lo > hi || !tail) return fail(POSET_EINVAL, "poset_scan_slots_mc: bad range");
+    CK(cudaSetDevice(h->device));
+    if ((st = check_split("poset_scan_slots_mc", {f}, {tail}))) return st;
+    if ((uintptr_t)F_mc % 8) return fail(POSET_EINVAL, "poset_scan_slots_mc: F_mc must be 8-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = begin_call(h, s))) return st;
+    st = grow(h, &h->d_scan, &h->scan_bytes, scan_scratch_bytes(hi - lo, batch));
+    if (st) return st;
+    CK(launch_scan(h->dev(), dt, f, nullptr, lo, hi, batch, h->d_scan, tail, s, F_mc));
+    return end_call(h, s, POSET_OK);
+}
+
 poset_status poset_scan_slots(poset_t h, const void *f, void *F, void *tail, int64_t lo, int64_t hi,
                               int64_t batch, poset_dtype dt, void *stream) {
     poset_status st = check_call(h, f, F, batch, dt, "poset_scan_slots");
@@ -1163,6 +1180,194 @@ const char *poset_strerror(poset_status s) {
 }
 
 const char *poset_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"
+
+// ---------------------------------------------- NVLS multicast buffers ----
+// Driver entry points fetched through the runtime (no link against libcuda).
+namespace {
+struct Drv {
+    bool ok = false;
+    decltype(&cuDeviceGet) DeviceGet;
+    decltype(&cuMulticastCreate) McCreate;
+    decltype(&cuMulticastGetGranularity) McGran;
+    decltype(&cuMulticastAddDevice) McAdd;
+    decltype(&cuMulticastBindMem) McBind;
+    decltype(&cuMulticastUnbind) McUnbind;
+    decltype(&cuMemGetAllocationGranularity) MemGran;
+    decltype(&cuMemCreate) MemCreate;
+    decltype(&cuMemRelease) MemRelease;
+    decltype(&cuMemAddressReserve) AddrReserve;
+    decltype(&cuMemAddressFree) AddrFree;
+    decltype(&cuMemMap) Map;
+    decltype(&cuMemUnmap) Unmap;
+    decltype(&cuMemSetAccess) SetAccess;
+    decltype(&cuDeviceGetAttribute) DevAttr;
+};
+template <class F>
+bool entry(const char *name, F &fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion(name, &p, 12030, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p) {
+        cudaGetLastError();
+        return false;
+    }
+    fn = reinterpret_cast<F>(p);
+    return true;
+}
+const Drv &drv() {
+    static Drv d = [] {
+        Drv x;
+        x.ok = entry("cuDeviceGet", x.DeviceGet) && entry("cuMulticastCreate", x.McCreate) &&
+               entry("cuMulticastGetGranularity", x.McGran) && entry("cuMulticastAddDevice", x.McAdd) &&
+               entry("cuMulticastBindMem", x.McBind) && entry("cuMulticastUnbind", x.McUnbind) &&
+               entry("cuMemGetAllocationGranularity", x.MemGran) && entry("cuMemCreate", x.MemCreate) &&
+               entry("cuMemRelease", x.MemRelease) && entry("cuMemAddressReserve", x.AddrReserve) &&
+               entry("cuMemAddressFree", x.AddrFree) && entry("cuMemMap", x.Map) && entry("cuMemUnmap", x.Unmap) &&
+               entry("cuMemSetAccess", x.SetAccess) && entry("cuDeviceGetAttribute", x.DevAttr);
+        return x;
+    }();
+    return d;
+}
+}  // namespace
+
+struct poset_nvls_s {
+    int ndev = 0;
+    std::vector<int> dev;
+    size_t size = 0;
+    CUmemGenericAllocationHandle mc = 0;
+    std::vector<CUmemGenericAllocationHandle> mem;
+    std::vector<CUdeviceptr> uc;
+    CUdeviceptr mcva = 0;
+    std::vector<bool> bound, mapped;
+    bool mc_mapped = false;
+};
+
+static void nvls_release(poset_nvls_s *b) {
+    const Drv &d = drv();
+    if (!b || !d.ok) return;
+    if (b->mc_mapped) { d.Unmap(b->mcva, b->size); }
+    if (b->mcva) d.AddrFree(b->mcva, b->size);
+    for (int i = 0; i < b->ndev; i++) {
+        if (b->mapped[i]) d.Unmap(b->uc[i], b->size);
+        if (b->uc[i]) d.AddrFree(b->uc[i], b->size);
+        if (b->bound[i]) {
+            CUdevice cd;
+            if (d.DeviceGet(&cd, b->dev[i]) == CUDA_SUCCESS) d.McUnbind(b->mc, cd, 0, b->size);
+        }
+        if (b->mem[i]) d.MemRelease(b->mem[i]);
+    }
+    if (b->mc) d.MemRelease(b->mc);
+}
+
+#define CU(expr, what)                                                                           \
+    do {                                                                                         \
+        CUresult _r = (expr);                                                                    \
+        if (_r != CUDA_SUCCESS) {                                                                \
+            nvls_release(b);                                                                     \
+            delete b;                                                                            \
+            return fail(_r == CUDA_ERROR_OUT_OF_MEMORY ? POSET_ENOMEM : POSET_ECUDA,             \
+                        std::string("poset_nvls_create: ") + what + " failed (CUresult " +       \
+                            std::to_string((int)_r) + ")");                                      \
+        }                                                                                        \
+    } while (0)
+
+extern "C" {
+
+poset_status poset_nvls_create(const int *devices, int ndev, int64_t bytes, poset_nvls_t *out) {
+    if (!out || !devices || ndev < 1 || ndev > 64 || bytes <= 0)
+        return fail(POSET_EINVAL, "poset_nvls_create: bad argument");
+    *out = nullptr;
+    const Drv &d = drv();
+    if (!d.ok) return fail(POSET_ECUDA, "poset_nvls_create: driver multicast entry points unavailable");
+    poset_nvls_s *b = new poset_nvls_s();
+    b->ndev = ndev;
+    b->dev.assign(devices, devices + ndev);
+    b->mem.assign(ndev, 0);
+    b->uc.assign(ndev, 0);
+    b->bound.assign(ndev, false);
+    b->mapped.assign(ndev, false);
+    std::vector<CUdevice> cd(ndev);
+    for (int i = 0; i < ndev; i++) {
+        if (cudaSetDevice(devices[i]) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) {   // context
+            cudaGetLastError();
+            delete b;
+            return fail(POSET_EINVAL, "poset_nvls_create: bad device ordinal");
+        }
+        CU(d.DeviceGet(&cd[i], devices[i]), "cuDeviceGet");
+        int sup = 0;
+        CU(d.DevAttr(&sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd[i]), "cuDeviceGetAttribute");
+        if (!sup) {
+            delete b;
+            return fail(POSET_ECUDA, "poset_nvls_create: device does not support multicast (NVLS)");
+        }
+    }
+    // the driver wants an exportable handle type on the object (the POSIX fd
+    // type; nothing is exported here), NONE as a fallback
+    CUmulticastObjectProp mp = {};
+    mp.numDevices = (unsigned)ndev;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = (size_t)bytes;
+    size_t mg = 0, ag = 0;
+    CU(d.McGran(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
+    CUmemAllocationProp ap = {};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = devices[0];
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    CU(d.MemGran(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+    const size_t gran = std::max(mg, ag);
+    b->size = ((size_t)bytes + gran - 1) / gran * gran;
+    mp.size = b->size;
+    if (d.McCreate(&b->mc, &mp) != CUDA_SUCCESS) {
+        b->mc = 0;
+        mp.handleTypes = CU_MEM_HANDLE_TYPE_NONE;
+        ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+        CU(d.McCreate(&b->mc, &mp), "cuMulticastCreate");
+    }
+    for (int i = 0; i < ndev; i++) CU(d.McAdd(b->mc, cd[i]), "cuMulticastAddDevice");
+    std::vector<CUmemAccessDesc> acc(ndev);
+    for (int i = 0; i < ndev; i++) {
+        acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc[i].location.id = devices[i];
+        acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    for (int i = 0; i < ndev; i++) {
+        cudaSetDevice(devices[i]);
+        ap.location.id = devices[i];
+        CU(d.MemCreate(&b->mem[i], b->size, &ap, 0), "cuMemCreate");
+        CU(d.McBind(b->mc, 0, b->mem[i], 0, b->size, 0), "cuMulticastBindMem");
+        b->bound[i] = true;
+        CU(d.AddrReserve(&b->uc[i], b->size, gran, 0, 0), "cuMemAddressReserve");
+        CU(d.Map(b->uc[i], b->size, 0, b->mem[i], 0), "cuMemMap");
+        b->mapped[i] = true;
+        CU(d.SetAccess(b->uc[i], b->size, &acc[i], 1), "cuMemSetAccess");
+    }
+    CU(d.AddrReserve(&b->mcva, b->size, gran, 0, 0), "cuMemAddressReserve (multicast)");
+    CU(d.Map(b->mcva, b->size, 0, b->mc, 0), "cuMemMap (multicast)");
+    b->mc_mapped = true;
+    CU(d.SetAccess(b->mcva, b->size, acc.data(), ndev), "cuMemSetAccess (multicast)");
+    cudaSetDevice(devices[0]);
+    *out = b;
+    return POSET_OK;
+}
+
+poset_status poset_nvls_ptrs(poset_nvls_t b, void **mc, void **uc, int64_t *bytes) {
+    if (!b) return fail(POSET_EINVAL, "poset_nvls_ptrs: null buffer");
+    if (mc) *mc = (void *)b->mcva;
+    if (uc)
+        for (int i = 0; i < b->ndev; i++) uc[i] = (void *)b->uc[i];
+    if (bytes) *bytes = (int64_t)b->size;
+    return POSET_OK;
+}
+
+void poset_nvls_destroy(poset_nvls_t b) {
+    if (!b) return;
+    cudaDeviceSynchronize();
+    nvls_release(b);
+    delete b;
+}
 
 int poset_abi_version(void) { return 2; }   // 2: poset_info.moebius_sms / num_sms
 

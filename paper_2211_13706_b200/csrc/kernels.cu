@@ -349,12 +349,20 @@ __device__ __forceinline__ void seg_block_scan(T &v, int &fl, int rg, int bl, in
     __syncthreads();
 }
 
+// NVLS multicast store: one st through the multicast
+// address reaches the same offset of every device's buffer bound to the
+// multicast object (NVSwitch replicates it) -- the all-gather of F fused into
+// the scan epilogue.
+__device__ __forceinline__ void mc_st64(void *p, unsigned long long v) {
+    asm volatile("multimem.st.weak.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_scan_tiles(const T *__restrict__ f, T *__restrict__ F,
                                                     const int32_t *__restrict__ slot_user,
                                                     int64_t lo, int64_t rows, int32_t B, int CB,
                                                     int RG, int R, T *agg_v, int *agg_f,
-                                                    const T *carry, int phase) {
+                                                    const T *carry, int phase, T *Fmc = nullptr) {
     __shared__ T sv[256];
     __shared__ int sf[256];
     const int bl = threadIdx.x % CB, rg = threadIdx.x / CB;
@@ -396,8 +404,10 @@ __global__ void __launch_bounds__(256) k_scan_tiles(const T *__restrict__ f, T *
         int32_t u = slot_user[s];
         if (u < 0) run = T(0);
         run += f[(size_t)(u & 0x7fffffff) * B + b];
-        F[(size_t)s * B + b] = run;
+        if (Fmc) mc_st64(Fmc + (size_t)s * B + b, to_bits<T>(run));
+        else F[(size_t)s * B + b] = run;
     }
+    if (Fmc) __threadfence_system();   // the rows are visible to every peer at kernel end
 }
 
 // carry[t] = value of the exclusive segmented prefix over tiles < t (per column)
@@ -438,7 +448,7 @@ __global__ void __launch_bounds__(1024) k_scan_carry_tiles(const T *agg_v, const
 
 template <typename T>
 static cudaError_t scan_t(const DevPoset &P, const void *f, void *F, int64_t lo, int64_t hi,
-                          int64_t B, void *scratch, void *tail, cudaStream_t s) {
+                          int64_t B, void *scratch, void *tail, cudaStream_t s, void *Fmc) {
     const int64_t rows = hi - lo;
     if (rows <= 0) {
         if (tail) return cudaMemsetAsync(tail, 0, sizeof(T) * 2 * B, s);
@@ -454,15 +464,15 @@ static cudaError_t scan_t(const DevPoset &P, const void *f, void *F, int64_t lo,
     k_scan_carry_tiles<T><<<(unsigned)B, 1024, 0, s>>>(agg_v, agg_f, carry, g.ntiles, (int32_t)B,
                                                        (T *)tail);
     k_scan_tiles<T><<<grid, 256, 0, s>>>((const T *)f, (T *)F, P.slot_user, lo, rows, (int32_t)B,
-                                         g.CB, g.RG, g.R, agg_v, agg_f, carry, 3);
+                                         g.CB, g.RG, g.R, agg_v, agg_f, carry, 3, (T *)Fmc);
     COUNT_LAUNCH(3);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan(const DevPoset &P, int dtype, const void *f, void *F, int64_t lo,
-                        int64_t hi, int64_t B, void *scratch, void *tail, cudaStream_t s) {
-    return dtype == 0 ? scan_t<u64>(P, f, F, lo, hi, B, scratch, tail, s)
-                      : scan_t<double>(P, f, F, lo, hi, B, scratch, tail, s);
+                        int64_t hi, int64_t B, void *scratch, void *tail, cudaStream_t s, void *Fmc) {
+    return dtype == 0 ? scan_t<u64>(P, f, F, lo, hi, B, scratch, tail, s, Fmc)
+                      : scan_t<double>(P, f, F, lo, hi, B, scratch, tail, s, Fmc);
 }
 
 // ---------------------------------------- (iii) single-pass scan (zeta) ----

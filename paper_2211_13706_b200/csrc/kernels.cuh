@@ -46,7 +46,7 @@ cudaError_t launch_depth_u(const DevPoset &P, const int32_t *slot_rank, int32_t 
 size_t scan_scratch_bytes(int64_t rows, int64_t batch);
 cudaError_t launch_scan(const DevPoset &P, int dtype, const void *f, void *F, int64_t slot_lo,
                         int64_t slot_hi, int64_t batch, void *scratch, void *tail,
-                        cudaStream_t s);
+                        cudaStream_t s, void *F_mc = nullptr);   // F_mc: NVLS multicast stores
 // The whole slot range in one pass (decoupled look-back, f read once): the
 // zeta transform's scan.  scratch: scan1p_scratch_bytes(n, batch) bytes.
 size_t scan1p_scratch_bytes(int64_t rows, int64_t batch);

@@ -133,3 +133,71 @@ def emulate_row_sharded_zeta(P, f, world: int):
     out = torch.empty_like(f2)
     P.rank_to_user(g_rank[:n].contiguous(), out)
     return out.reshape(f.shape)
+
+
+def nvls_buffer_bytes(n: int, world: int, batch: int) -> int:
+    """Bytes of the F buffer ``nvls_row_sharded_zeta`` views: world·chunk + 1
+    rows (the zero row n) of ``batch`` 8-byte values."""
+    chunk = shard_range(n, world, 0)[2]
+    return (world * chunk + 1) * batch * 8
+
+
+def nvls_row_sharded_zeta(Ps, fs, buf, out=None):
+    """Row-sharded zeta with the all-gather of F fused into the scan (SURVEY
+    §8(f) N3): "rank" p -- handle ``Ps[p]``, replicated input ``fs[p]`` on
+    its device -- scans its slot range with ``poset_scan_slots_mc``, whose
+    every F row goes through the NVLS multicast address ``buf.mc`` and so
+    lands on every device bound to ``buf`` (no F all-gather follows).  Each
+    device then applies every range's carry (``poset_combine_tails`` over the
+    per-range scan tails, then ``poset_scan_carry``; only the rows before a
+    range's first chain start change) to its own copy, zeroes row n, and rank
+    p gathers its rank rows [lo_p, hi_p) (kernel iv).  g is assembled in user
+    order on ``fs[0]``'s device.
+
+    One process drives all ranks: ``buf.devices`` lists one device per rank
+    (multi-GPU), or one device for all ranks (emulated ranks sharing one F,
+    the 1-GPU test).  Cross-process sharing of the multicast object (one
+    process per GPU) is not built (include/poset.h)."""
+    import torch
+    world = len(Ps)
+    P0 = Ps[0]
+    n = P0.n
+    B = fs[0].reshape(n, -1).shape[1]
+    dt = fs[0].dtype
+    chunk = shard_range(n, world, 0)[2]
+    shared = len(buf.devices) == 1
+    if not shared and len(buf.devices) != world:
+        raise ValueError("buf.devices: one device per rank, or one device for all ranks")
+    bidx = [0 if shared else p for p in range(world)]
+    Fs = {d: buf.tensor(d, (world * chunk + 1, B), dt) for d in sorted(set(bidx))}
+    tails = []
+    for p in range(world):
+        lo, hi, _ = shard_range(n, world, p)
+        f2 = fs[p].reshape(n, -1)
+        tail = torch.zeros((2, B), dtype=dt, device=f2.device)
+        Ps[p].scan_slots_mc(f2, buf.mc, tail, lo, hi)
+        tails.append(tail)
+    for d in buf.devices:   # every rank's multicast stores have landed everywhere
+        torch.cuda.synchronize(d)
+    for d, F in Fs.items():
+        Pd = Ps[bidx.index(d)]
+        tails_all = torch.stack([t.to(F.device) for t in tails]).contiguous()
+        for p in range(world):
+            lo, hi, _ = shard_range(n, world, p)
+            carry = torch.zeros((B,), dtype=dt, device=F.device)
+            Pd.combine_tails(tails_all, world, p, carry)
+            Pd.scan_carry(F, carry, lo, hi)
+        F[n].zero_()
+    dev0 = fs[0].device
+    g_rank = torch.zeros((world * chunk, B), dtype=dt, device=dev0)
+    for p in range(world):
+        lo, hi, _ = shard_range(n, world, p)
+        if hi > lo:
+            F = Fs[bidx[p]]
+            part = torch.zeros((chunk, B), dtype=dt, device=F.device)
+            Ps[p].gather_rows(F, part, lo, hi)
+            g_rank[p * chunk:(p + 1) * chunk] = part.to(dev0)
+    if out is None:
+        out = torch.empty((n, B), dtype=dt, device=dev0)
+    P0.rank_to_user(g_rank[:n].contiguous(), out)
+    return out.reshape(fs[0].shape)

@@ -683,3 +683,30 @@ def test_pipelined_zeta_and_moebius_on_two_streams():
         assert (gpu_zeta(P, fs[3]) == O.zeta(fs[3])).all()
     finally:
         P.set_option("zeta_sms", 0)
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_nvls_fused_scan_row_sharded_zeta(G):
+    """the row-sharded zeta with the F all-gather fused into
+    the scan epilogue -- every F row stored with multimem.st through an NVLS
+    multicast address (poset_scan_slots_mc) -- for G emulated ranks on one
+    GPU (all bound to the one device's buffer), vs O2: int64 bit-exact, fp64
+    within the tolerance.  Skips when the driver / device has no multicast."""
+    from paper_2211_13706_b200 import dist as pdist
+    n = 30011
+    src, dst = W.window_dag(n, 2, 64, 7, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    try:
+        buf = pz.NvlsBuffer([0], pdist.nvls_buffer_bytes(n, G, 8))
+    except pz.PosetError as e:   # pragma: no cover - depends on the box
+        pytest.skip(f"no NVLS multicast here: {e}")
+    try:
+        for B in (1, 3, 8):
+            f = W.int_values(n, B, -10**15, 10**15, seed=B + 60)
+            g = pdist.nvls_row_sharded_zeta([P] * G, [dev(f)] * G, buf)
+            assert (host(g) == O.zeta(f)).all(), B
+        ff = W.normal_values(n, 2, seed=9)
+        g = pdist.nvls_row_sharded_zeta([P] * G, [dev(ff)] * G, buf)
+        assert_fp64_close(host(g), O.zeta(ff), O.zeta(np.abs(ff)))
+    finally:
+        buf.close()
