@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
                     help="batched pipeline: batch i+1's zeta on the SMs batch i's ring-family Möbius "
                          "leaves free (two streams; auto = when the Möbius leaves SMs free)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
     ap.add_argument("--no-e2e", action="store_true")
@@ -343,7 +343,10 @@ def main():
     zeta_budget = max(free_sms, 1) if use_pipe else 0
     if use_pipe:
         s_z = torch.cuda.Stream(priority=0)
-        s_m = torch.cuda.Stream(priority=-1)
+        # two Möbius streams, alternating: batch i+1's permutation kernel
+        # (its own rank-major buffer) runs while batch i's solve is still on
+        # the SMs; the library keeps the solves themselves one at a time
+        s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
         gb = [g, torch.empty_like(x)]
         ev_z = [torch.cuda.Event(), torch.cuda.Event()]
         ev_m = [torch.cuda.Event(), torch.cuda.Event()]
@@ -355,22 +358,24 @@ def main():
             return
         cur = torch.cuda.current_stream()
         s_z.wait_stream(cur)
-        s_m.wait_stream(cur)
+        for sm in s_m:
+            sm.wait_stream(cur)
         P.set_option("zeta_sms", 0)            # the prologue zeta has the whole GPU
         P.zeta(x, out=gb[0], stream=s_z)
         ev_z[0].record(s_z)
         P.set_option("zeta_sms", zeta_budget)
         for i in range(nsteps):
             b = i % 2
-            s_m.wait_event(ev_z[b])
-            P.moebius(gb[b], out=y, stream=s_m)
-            ev_m[b].record(s_m)
+            s_m[b].wait_event(ev_z[b])
+            P.moebius(gb[b], out=y, stream=s_m[b])
+            ev_m[b].record(s_m[b])
             if i + 1 < nsteps:
                 if i >= 1:                      # gb[1-b] was Möbius(i-1)'s input
                     s_z.wait_event(ev_m[1 - b])
                 P.zeta(x, out=gb[1 - b], stream=s_z)
                 ev_z[1 - b].record(s_z)
-        cur.wait_stream(s_m)
+        for sm in s_m:
+            cur.wait_stream(sm)
         cur.wait_stream(s_z)
         P.set_option("zeta_sms", 0)
 
@@ -509,7 +514,7 @@ def main():
         K = args.e2e_steps
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         # pipelined: the Möbius on its own high-priority stream (see run_steps)
-        s_mb = torch.cuda.Stream(priority=-1) if use_pipe else s_cmp
+        s_mb = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)] if use_pipe else [s_cmp] * 2
         xin = [torch.empty_like(x) for _ in range(2)]
         yout = [torch.empty_like(x) for _ in range(2)]
         gd2 = [torch.empty_like(x) for _ in range(2)] if use_pipe else [torch.empty_like(x)] * 2
@@ -534,12 +539,12 @@ def main():
                 P.zeta(xin[sl], out=gd2[sl], stream=s_cmp)
                 in_free[sl].record(s_cmp)
                 z_done[sl].record(s_cmp)
-                s_mb.wait_event(z_done[sl])
+                s_mb[sl].wait_event(z_done[sl])
                 if i >= 2:
-                    s_mb.wait_event(out_free[sl])
-                P.moebius(gd2[sl], out=yout[sl], stream=s_mb)
-                g_free[sl].record(s_mb)
-                out_done[sl].record(s_mb)
+                    s_mb[sl].wait_event(out_free[sl])
+                P.moebius(gd2[sl], out=yout[sl], stream=s_mb[sl])
+                g_free[sl].record(s_mb[sl])
+                out_done[sl].record(s_mb[sl])
                 with torch.cuda.stream(s_out):
                     s_out.wait_event(out_done[sl])
                     res[sl].copy_(yout[sl], non_blocking=True)
@@ -557,7 +562,8 @@ def main():
         a0.record(s_in)
         pipelined(K)
         s_in.wait_stream(s_out)
-        s_in.wait_stream(s_mb)
+        for sm in s_mb:
+            s_in.wait_stream(sm)
         a1.record(s_in)
         torch.cuda.synchronize()
         ems = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")

@@ -30,14 +30,20 @@
  *  Threads    a handle is not re-entrant: serialise calls per handle (host
  *             side).  Calls on DIFFERENT streams are ordered by the library
  *             wherever they share handle scratch: the scratch is split in
- *             three lanes (Z: the zeta's scan / gather buffers and the
- *             non-ring Möbius schedules; R: the ring-family Möbius input;
- *             S: host staging); each call records an event per lane it uses
- *             on its stream, and a call on another stream first waits on the
- *             events of its own lanes.  So a zeta on one stream and a
- *             ring-family Möbius (poset_info.moebius_kernel RING / RINGWS /
- *             RINGDF / RINGCL / RINGCW) on another, both on device buffers,
- *             run concurrently; everything else is serialised.  Data
+ *             lanes (Z: the zeta's scan / gather buffers and the non-ring
+ *             Möbius schedules; R0 / R1: the ring-family Möbius input, double
+ *             buffered -- a ring-family call on another stream than the
+ *             previous one takes the other buffer; S: host staging); each
+ *             call records an event per lane it uses on its stream, and a
+ *             call on another stream first waits on the events of its own
+ *             lanes.  So a zeta on one stream and a ring-family Möbius
+ *             (poset_info.moebius_kernel RING / RINGWS / RINGDF / RINGCL /
+ *             RINGCW) on another, both on device buffers, run concurrently,
+ *             and two ring-family Möbius calls on two streams overlap the
+ *             second one's permutation kernel with the first one's solve;
+ *             the solve kernels of one handle always run one at a time (the
+ *             library orders them by an event); everything else is
+ *             serialised.  Data
  *             dependencies between the caller's own buffers are the caller's
  *             to order (events).  A host result is valid once `stream` has
  *             synchronised (poset_sync).

@@ -38,10 +38,21 @@ struct poset_s {
     // buffer is shared by two calls in flight, while a zeta (lane Z) and a
     // ring-family Möbius (lane R) on two streams may run concurrently
     //   lane Z: d_F, d_scan, d_part, d_bar, the lazily built gather order;
-    //   lane R: d_gP (rank-major g of the ring schedules);  lane S: d_stage
-    cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
-    cudaStream_t lane_s[3] = {nullptr, nullptr, nullptr};
-    bool lane_used[3] = {false, false, false};
+    //   lanes R0 / R1: d_gPx[0] / [1] (rank-major g of the ring schedules,
+    //   double-buffered: a ring-family call on another stream than the
+    //   previous one takes the other buffer, so its permutation kernel runs
+    //   while the previous solve still reads the first);  lane S: d_stage
+    cudaEvent_t lane_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t lane_s[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool lane_used[4] = {false, false, false, false};
+    // the ring-family solve kernels of a handle run one at a time (each
+    // holds one cluster of SMs per column for the whole solve)
+    cudaEvent_t solve_ev = nullptr;
+    cudaStream_t solve_s = nullptr;
+    bool solve_used = false;
+    int gp_cur = 0;                   // d_gPx buffer of the current ring-family call
+    cudaStream_t gp_last_s = nullptr;
+    bool gp_any = false;
     int zeta_sms = 0;                 // option zeta_sms: SMs the zeta's persistent grids size for
     // device residency
     int32_t *d_rank_user = nullptr, *d_slot = nullptr, *d_chain = nullptr, *d_lvl = nullptr;
@@ -62,8 +73,8 @@ struct poset_s {
     bool sharded = false;
     int64_t m_lo = 0, m_hi = 0;
     bool gpi_delta_failed = false;
-    void *d_gP = nullptr;             // [B][npad] g in rank order (RING input)
-    size_t gP_bytes = 0;
+    void *d_gPx[2] = {nullptr, nullptr};   // [B][npad] g in rank order (ring-family input)
+    size_t gPx_bytes[2] = {0, 0};
     // scratch, grown on demand
     void *d_F = nullptr;
     size_t F_bytes = 0;
@@ -136,10 +147,11 @@ static void free_all(poset_s *h) {
     for (auto e : h->pool) cudaEventDestroy(e);
     for (auto e : h->lane_ev)
         if (e) cudaEventDestroy(e);
+    if (h->solve_ev) cudaEventDestroy(h->solve_ev);
     free_gather_pi(h->gpi);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gP, h->ring.dbg, h->csr.ptr, h->csr.idx};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gPx[0], h->d_gPx[1], h->ring.dbg, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -169,6 +181,7 @@ static poset_status finish_setup_sparse(poset_s *h, double t0, size_t table, siz
     CK(upload(&h->d_child, H.child));
     CK(upload(&h->d_slot_user, H.slot_user));
     for (auto &e : h->lane_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->solve_ev, cudaEventDisableTiming));
     CK(cudaMalloc((void **)&h->d_bar, 64));
     CK(cudaMalloc((void **)&h->d_count, 64));
     int32_t *d_slot_chain = nullptr, *d_chain_off = nullptr;
@@ -247,6 +260,7 @@ static poset_status finish_setup(poset_s *h) {
     CK(upload(&h->d_child, H.child));
     CK(upload(&h->d_slot_user, H.slot_user));
     for (auto &e : h->lane_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->solve_ev, cudaEventDisableTiming));
     CK(cudaMalloc((void **)&h->d_bar, 64));
     CK(cudaMalloc((void **)&h->d_count, 64));
     CK(cudaMalloc((void **)&h->d_M, std::max<size_t>(table, 4)));
@@ -470,10 +484,10 @@ static bool is_device_ptr(const void *p) {
 // vector loads and stores need (the transforms stage anything else).
 static bool dev_aligned(const void *p) { return is_device_ptr(p) && ((uintptr_t)p % 32) == 0; }
 
-enum : unsigned { LANE_Z = 1, LANE_R = 2, LANE_S = 4, LANE_ALL = 7 };
+enum : unsigned { LANE_Z = 1, LANE_R = 2, LANE_S = 4, LANE_R1 = 8, LANE_ALL = 15 };
 
 static poset_status begin_call(poset_s *h, cudaStream_t s, unsigned lanes = LANE_ALL) {
-    for (int l = 0; l < 3; l++)
+    for (int l = 0; l < 4; l++)
         if ((lanes >> l & 1) && h->lane_used[l] && s != h->lane_s[l])
             CK(cudaStreamWaitEvent(s, h->lane_ev[l], 0));
     return POSET_OK;
@@ -481,7 +495,7 @@ static poset_status begin_call(poset_s *h, cudaStream_t s, unsigned lanes = LANE
 
 static poset_status end_call(poset_s *h, cudaStream_t s, poset_status st, unsigned lanes = LANE_ALL) {
     if (st != POSET_OK) return st;
-    for (int l = 0; l < 3; l++)
+    for (int l = 0; l < 4; l++)
         if (lanes >> l & 1) {
             CK(cudaEventRecord(h->lane_ev[l], s));
             h->lane_s[l] = s;
@@ -622,8 +636,22 @@ static bool ring_family(int which) {
            which == MOEB_RING;
 }
 
+// one ring-family solve at a time per handle (see poset_s::solve_ev)
+static poset_status solve_begin(poset_s *h, cudaStream_t s) {
+    if (h->solve_used && h->solve_s != s) CK(cudaStreamWaitEvent(s, h->solve_ev, 0));
+    return POSET_OK;
+}
+static poset_status solve_end(poset_s *h, cudaStream_t s) {
+    CK(cudaEventRecord(h->solve_ev, s));
+    h->solve_s = s;
+    h->solve_used = true;
+    return POSET_OK;
+}
+
 static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, int dt, cudaStream_t s) {
     poset_status st = POSET_OK;
+    void *&d_gP = h->d_gPx[h->gp_cur];
+    size_t &gP_bytes = h->gPx_bytes[h->gp_cur];
     DevPoset P = h->dev();
     const int which = moebius_which(h, B);
     if (!ring_family(which) && (st = ensure_F(h, B, s))) return st;
@@ -651,55 +679,58 @@ static poset_status moebius_dev(poset_s *h, const void *g, void *f, int64_t B, i
             return fail(POSET_EINVAL, "poset_moebius: the RINGCL schedule does not fit this poset; use AUTO");
         if (which == MOEB_RINGCW && !ringcw_fits(h->rdf))
             return fail(POSET_EINVAL, "poset_moebius: the RINGCW schedule does not fit this poset; use AUTO");
-        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rdf.npad * 8);
+        st = grow(h, &d_gP, &gP_bytes, (size_t)B * h->rdf.npad * 8);
         if (st) return st;
         {
             PhaseTimer t(h, POSET_PH_PERM, s);
-            CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, h->d_gP, s));
+            CK(launch_to_rank_major(P, dt, g, B, h->rdf.npad, d_gP, s));
         }
+        if ((st = solve_begin(h, s))) return st;
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
         if (which == MOEB_RINGCL || which == MOEB_RINGCW) {
             h->rdf.cw = which == MOEB_RINGCW;
             int ctas = 0;
-            cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, h->num_sms, s,
+            cudaError_t ce = launch_moebius_ringcl(P, h->rdf, h->ring.ru_pad, dt, d_gP, f, B, h->num_sms, s,
                                                    &ctas);
             if (ce == cudaSuccess) h->info.moebius_sms = std::min(ctas, h->num_sms);
             if (ce == cudaErrorInvalidConfiguration && h->moeb_opt == MOEB_AUTO) {   // no cluster fits: RINGDF
                 cudaGetLastError();
                 h->info.moebius_kernel = MOEB_RINGDF;
-                ce = launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s);
+                ce = launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, d_gP, f, B, s);
             }
             CK(ce);
         } else
-            CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, h->d_gP, f, B, s));
-        return POSET_OK;
+            CK(launch_moebius_ringdf(P, h->rdf, h->ring.ru_pad, dt, d_gP, f, B, s));
+        return solve_end(h, s);
     }
     if (which == MOEB_RINGWS) {
         if (!h->rws.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RINGWS schedule does not fit this poset; use AUTO");
-        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->rws.npad * 8);
+        st = grow(h, &d_gP, &gP_bytes, (size_t)B * h->rws.npad * 8);
         if (st) return st;
         {
             PhaseTimer t(h, POSET_PH_PERM, s);
-            CK(launch_to_rank_major(P, dt, g, B, h->rws.npad, h->d_gP, s));
+            CK(launch_to_rank_major(P, dt, g, B, h->rws.npad, d_gP, s));
         }
+        if ((st = solve_begin(h, s))) return st;
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        CK(launch_moebius_ringws(P, h->rws, h->ring.ru_pad, dt, h->d_gP, f, B, s));
-        return POSET_OK;
+        CK(launch_moebius_ringws(P, h->rws, h->ring.ru_pad, dt, d_gP, f, B, s));
+        return solve_end(h, s);
     }
     if (which == MOEB_RING) {
         if (!h->ring.ok)
             return fail(POSET_EINVAL, "poset_moebius: the RING schedule does not fit this poset "
                                       "(reach or rows too large); use AUTO");
-        st = grow(h, &h->d_gP, &h->gP_bytes, (size_t)B * h->ring.npad * 8);
+        st = grow(h, &d_gP, &gP_bytes, (size_t)B * h->ring.npad * 8);
         if (st) return st;
         {
             PhaseTimer t(h, POSET_PH_PERM, s);
-            CK(launch_to_rank_major(P, dt, g, B, h->ring.npad, h->d_gP, s));
+            CK(launch_to_rank_major(P, dt, g, B, h->ring.npad, d_gP, s));
         }
+        if ((st = solve_begin(h, s))) return st;
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
-        CK(launch_moebius_ring(P, h->ring, dt, h->d_gP, f, B, s));
-        return POSET_OK;
+        CK(launch_moebius_ring(P, h->ring, dt, d_gP, f, B, s));
+        return solve_end(h, s);
     }
     {
         PhaseTimer t(h, POSET_PH_MSOLVE, s);
@@ -766,8 +797,13 @@ poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, pos
     if (st || h->H.n == 0) return st;
     CK(cudaSetDevice(h->device));
     cudaStream_t s = (cudaStream_t)stream;
-    const unsigned lanes = (ring_family(moebius_which(h, batch)) ? LANE_R : LANE_Z) |
-                           (needs_staging(g, f) ? LANE_S : 0);
+    const bool ringf = ring_family(moebius_which(h, batch));
+    if (ringf) {   // the other rank-major buffer when the stream changes (see poset_s::d_gPx)
+        if (h->gp_any && s != h->gp_last_s) h->gp_cur ^= 1;
+        h->gp_last_s = s;
+        h->gp_any = true;
+    }
+    const unsigned lanes = (ringf ? (h->gp_cur ? LANE_R1 : LANE_R) : LANE_Z) | (needs_staging(g, f) ? LANE_S : 0);
     if ((st = begin_call(h, s, lanes))) return st;
     return end_call(h, s, run_staged(h, moebius_dev, g, f, batch, dt, s), lanes);
 }

@@ -655,17 +655,18 @@ def test_pipelined_zeta_and_moebius_on_two_streams():
     P.set_option("zeta_sms", info["num_sms"] - info["moebius_sms"])
     try:
         cur = torch.cuda.current_stream()
-        s_z, s_m = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
-        s_z.wait_stream(cur)
-        s_m.wait_stream(cur)
+        s_z = torch.cuda.Stream(priority=0)
+        s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
+        for st in (s_z, *s_m):
+            st.wait_stream(cur)
         gs = [torch.empty_like(x) for x in xs]
         ys = [torch.empty_like(x) for x in xs]
         ev = [torch.cuda.Event() for _ in xs]
-        for i, x in enumerate(xs):        # zeta i+1.. queue behind zeta i, Möbius i overlaps them
-            P.zeta(x, out=gs[i], stream=s_z)
-            ev[i].record(s_z)
-            s_m.wait_event(ev[i])
-            P.moebius(gs[i], out=ys[i], stream=s_m)
+        for i, x in enumerate(xs):        # zeta i+1.. queue behind zeta i, Möbius i overlaps them;
+            P.zeta(x, out=gs[i], stream=s_z)   # Möbius on alternating streams (double-buffered
+            ev[i].record(s_z)                  # rank-major g, solves ordered by the library)
+            s_m[i % 2].wait_event(ev[i])
+            P.moebius(gs[i], out=ys[i], stream=s_m[i % 2])
         torch.cuda.synchronize()
         for i, f in enumerate(fs):
             assert (host(gs[i]) == O.zeta(f)).all(), i
