@@ -133,3 +133,27 @@ def test_literal_configs_are_too_big_for_dense_table():
 def test_empty_poset():
     info = pz.analyze(0, np.zeros(0, np.int64), np.zeros(0, np.int64))
     assert info["n"] == 0 and info["k"] == 0 and info["ell"] == 0
+
+
+def test_nvls_and_fused_scan_argument_errors():
+    """The NVLS entry points (include/poset.h, N3) validate their arguments
+    before touching the driver: bad device lists / sizes and null handles
+    are EINVAL on a machine without a GPU too."""
+    import ctypes
+    h = ctypes.c_void_p()
+    devs = (ctypes.c_int * 1)(0)
+    assert pz.STATUS[pz.lib.poset_nvls_create(devs, 0, 1 << 20, ctypes.byref(h))] == "EINVAL"
+    assert pz.STATUS[pz.lib.poset_nvls_create(devs, 1, 0, ctypes.byref(h))] == "EINVAL"
+    assert pz.STATUS[pz.lib.poset_nvls_create(None, 1, 1 << 20, ctypes.byref(h))] == "EINVAL"
+    assert pz.STATUS[pz.lib.poset_nvls_create(devs, 1, 1 << 20, None)] == "EINVAL"
+    assert pz.STATUS[pz.lib.poset_nvls_ptrs(None, None, None, None)] == "EINVAL"
+    pz.lib.poset_nvls_destroy(None)                       # no-op
+    assert pz.STATUS[pz.lib.poset_scan_slots_mc(None, None, None, None, 0, 0, 1, 0, None)] == "EINVAL"
+
+
+def test_binding_abi_version_and_info_layout():
+    """The binding marshals poset_info with the layout of ABI 2 (the
+    pipeline fields moebius_sms / num_sms at the end)."""
+    assert pz.ABI_VERSION == pz.lib.poset_abi_version() == 2
+    names = [f for f, _ in pz.PosetInfo._fields_]
+    assert names[-2:] == ["moebius_sms", "num_sms"]
