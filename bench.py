@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
                     help="batched pipeline: batch i+1's zeta on the SMs batch i's ring-family Möbius "
                          "leaves free (two streams; auto = when the Möbius leaves SMs free)")
+    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
+                    help="Möbius solves in flight in the pipeline (2: one helper SM per column, two "
+                         "batches' solves overlap; a throughput option, not the default)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
@@ -333,11 +336,14 @@ def main():
     # Möbius use disjoint lanes, include/poset.h).  The Möbius stream has the
     # higher priority so its clusters are placed before the zeta's CTAs; the
     # zeta's persistent gather grid is sized to the free SMs (option zeta_sms).
+    if args.inflight == 2:
+        P.set_option("ringcl_helpers", 1)
+        P.set_option("solves_inflight", 2)
     step()   # first call: builds the lazy tables and resolves the Möbius footprint
     torch.cuda.synchronize()
     inf0 = P.info()
     ring_fam = MOEB_NAMES[inf0["moebius_kernel"]] in ("ring", "ringws", "ringdf", "ringcl", "ringcw")
-    free_sms = inf0["num_sms"] - inf0["moebius_sms"]
+    free_sms = inf0["num_sms"] - args.inflight * inf0["moebius_sms"]
     use_pipe = (not row_mode and B > 0 and ring_fam and free_sms >= 8 and args.pipeline != "off") or \
         (args.pipeline == "on" and not row_mode and B > 0)
     zeta_budget = max(free_sms, 1) if use_pipe else 0
@@ -347,9 +353,11 @@ def main():
         # (its own rank-major buffer) runs while batch i's solve is still on
         # the SMs; the library keeps the solves themselves one at a time
         s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
-        gb = [g, torch.empty_like(x)]
-        ev_z = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_m = [torch.cuda.Event(), torch.cuda.Event()]
+        NB = 2 + (args.inflight - 1)           # g buffers: one per batch between zeta and Möbius
+        gb = [g] + [torch.empty_like(x) for _ in range(NB - 1)]
+        ys = [y, torch.empty_like(x)] if args.inflight == 2 else [y, y]
+        ev_z = [torch.cuda.Event() for _ in range(NB)]
+        ev_m = [torch.cuda.Event() for _ in range(NB)]
 
     def run_steps(nsteps):
         if not use_pipe:
@@ -365,15 +373,16 @@ def main():
         ev_z[0].record(s_z)
         P.set_option("zeta_sms", zeta_budget)
         for i in range(nsteps):
-            b = i % 2
-            s_m[b].wait_event(ev_z[b])
-            P.moebius(gb[b], out=y, stream=s_m[b])
-            ev_m[b].record(s_m[b])
+            b, sm = i % NB, s_m[i % 2]
+            sm.wait_event(ev_z[b])
+            P.moebius(gb[b], out=ys[i % 2], stream=sm)
+            ev_m[b].record(sm)
             if i + 1 < nsteps:
-                if i >= 1:                      # gb[1-b] was Möbius(i-1)'s input
-                    s_z.wait_event(ev_m[1 - b])
-                P.zeta(x, out=gb[1 - b], stream=s_z)
-                ev_z[1 - b].record(s_z)
+                nb = (i + 1) % NB
+                if i + 1 >= NB:                 # gb[nb] was Möbius(i+1-NB)'s input
+                    s_z.wait_event(ev_m[nb])
+                P.zeta(x, out=gb[nb], stream=s_z)
+                ev_z[nb].record(s_z)
         for sm in s_m:
             cur.wait_stream(sm)
         cur.wait_stream(s_z)
@@ -383,7 +392,8 @@ def main():
     torch.cuda.synchronize()
     # correctness spot check of the timed computation (round trip)
     if wl.dtype == "i64":
-        ok = bool(torch.equal(y, x)) if (rank == 0 or not row_mode) else None
+        y_last = ys[(args.warmup - 1) % 2] if use_pipe and args.warmup > 0 else y
+        ok = bool(torch.equal(y_last, x)) if (rank == 0 or not row_mode) else None
     else:
         ok = None   # fp64 Möbius on deep posets is ill-conditioned (reading G8)
     P.set_option("profile", 1)
@@ -634,6 +644,7 @@ def main():
                                        if row_mode else f"column-shard x{world}"),
                        "depth_u": P.info()["depth_u"], "provenance": prov, "index_shard": shard,
                        "pipeline": ({"zeta_sms": zeta_budget, "moebius_sms": inf0["moebius_sms"],
+                                     "solves_inflight": args.inflight,
                                      "how": "batch i+1's zeta (low-priority stream, gather grid on the free "
                                             "SMs) overlaps batch i's Möbius (high-priority stream); every "
                                             "step still runs scan, gather, permutation and U-solve on its "

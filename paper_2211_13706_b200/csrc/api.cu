@@ -50,6 +50,7 @@ struct poset_s {
     cudaEvent_t solve_ev = nullptr;
     cudaStream_t solve_s = nullptr;
     bool solve_used = false;
+    int solves_inflight = 1;          // option solves_inflight (1: one solve at a time; 2: no ordering)
     int gp_cur = 0;                   // d_gPx buffer of the current ring-family call
     cudaStream_t gp_last_s = nullptr;
     bool gp_any = false;
@@ -638,6 +639,7 @@ static bool ring_family(int which) {
 
 // one ring-family solve at a time per handle (see poset_s::solve_ev)
 static poset_status solve_begin(poset_s *h, cudaStream_t s) {
+    if (h->solves_inflight >= 2) return POSET_OK;   // option solves_inflight: two streams' solves overlap
     if (h->solve_used && h->solve_s != s) CK(cudaStreamWaitEvent(s, h->solve_ev, 0));
     return POSET_OK;
 }
@@ -1036,6 +1038,11 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
                 return fail(POSET_EINVAL, "ringws_lpeo must leave 8 or 16 far entries per lane");
             h->rws.lpeo = (int32_t)value;
         }
+        return POSET_OK;
+    }
+    if (!strcmp(key, "solves_inflight")) {   // 2: ring-family solves on two streams may overlap
+        if (value < 1 || value > 2) return fail(POSET_EINVAL, "poset_set_option: solves_inflight is 1 or 2");
+        h->solves_inflight = (int)value;
         return POSET_OK;
     }
     if (!strcmp(key, "zeta_sms")) {   // SMs the zeta's persistent grids size for (0 = all)
