@@ -69,6 +69,7 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-inflight2", action="store_true", help="skip the two-solves-in-flight throughput leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-provenance", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="oracle prefix size")
@@ -353,13 +354,19 @@ def main():
         # (its own rank-major buffer) runs while batch i's solve is still on
         # the SMs; the library keeps the solves themselves one at a time
         s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
-        NB = 2 + (args.inflight - 1)           # g buffers: one per batch between zeta and Möbius
-        gb = [g] + [torch.empty_like(x) for _ in range(NB - 1)]
-        ys = [y, torch.empty_like(x)] if args.inflight == 2 else [y, y]
-        ev_z = [torch.cuda.Event() for _ in range(NB)]
-        ev_m = [torch.cuda.Event() for _ in range(NB)]
 
-    def run_steps(nsteps):
+    def make_pipe(inflight, budget):
+        NB = 2 + (inflight - 1)                # g buffers: one per batch between zeta and Möbius
+        return {"NB": NB, "budget": budget,
+                "gb": [g] + [torch.empty_like(x) for _ in range(NB - 1)],
+                "ys": [y, torch.empty_like(x)] if inflight == 2 else [y, y],
+                "ev_z": [torch.cuda.Event() for _ in range(NB)],
+                "ev_m": [torch.cuda.Event() for _ in range(NB)]}
+
+    pipe0 = make_pipe(args.inflight, zeta_budget) if use_pipe else None
+
+    def run_steps(nsteps, pipe=None):
+        pipe = pipe or pipe0
         if not use_pipe:
             for _ in range(nsteps):
                 step()
@@ -368,10 +375,11 @@ def main():
         s_z.wait_stream(cur)
         for sm in s_m:
             sm.wait_stream(cur)
+        NB, gb, ys, ev_z, ev_m = pipe["NB"], pipe["gb"], pipe["ys"], pipe["ev_z"], pipe["ev_m"]
         P.set_option("zeta_sms", 0)            # the prologue zeta has the whole GPU
         P.zeta(x, out=gb[0], stream=s_z)
         ev_z[0].record(s_z)
-        P.set_option("zeta_sms", zeta_budget)
+        P.set_option("zeta_sms", pipe["budget"])
         for i in range(nsteps):
             b, sm = i % NB, s_m[i % 2]
             sm.wait_event(ev_z[b])
@@ -392,7 +400,7 @@ def main():
     torch.cuda.synchronize()
     # correctness spot check of the timed computation (round trip)
     if wl.dtype == "i64":
-        y_last = ys[(args.warmup - 1) % 2] if use_pipe and args.warmup > 0 else y
+        y_last = pipe0["ys"][(args.warmup - 1) % 2] if use_pipe and args.warmup > 0 else y
         ok = bool(torch.equal(y_last, x)) if (rank == 0 or not row_mode) else None
     else:
         ok = None   # fp64 Möbius on deep posets is ill-conditioned (reading G8)
@@ -609,6 +617,43 @@ def main():
                                    "path": "poset_zeta and poset_moebius each host -> host (library-staged copies)"}
         del fp, gp
 
+    # throughput with two batches' solves in flight (option solves_inflight,
+    # DESIGN.md §5.5): one helper SM per column instead of two, so two RINGCL
+    # solves sit side by side and the zeta takes the remaining SMs.  Reported
+    # beside the headline (which keeps one solve at a time: lower per-batch
+    # latency, and the dominant kernel's launch duration is the roofline's).
+    two = None
+    if use_pipe and args.inflight == 1 and world == 1 and not args.no_inflight2 and \
+            MOEB_NAMES[inf0["moebius_kernel"]] == "ringcl":
+        try:
+            P.set_option("ringcl_helpers", 1)
+            P.set_option("solves_inflight", 2)
+            step()
+            torch.cuda.synchronize()
+            inf2 = P.info()
+            free2 = inf2["num_sms"] - 2 * inf2["moebius_sms"]
+            if free2 >= 8:
+                pipe2 = make_pipe(2, free2)
+                run_steps(3, pipe2)
+                torch.cuda.synchronize()
+                ok2 = bool(torch.equal(pipe2["ys"][0], x)) if wl.dtype == "i64" else None
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                b0.record()
+                run_steps(args.steps, pipe2)
+                b1.record()
+                torch.cuda.synchronize()
+                ms2 = b0.elapsed_time(b1)
+                two = {"ms_per_step": ms2 / args.steps, "value": units_step * args.steps / (ms2 / 1e3),
+                       "unit": "n·k·B gathers/s", "steps": args.steps, "solves_inflight": 2,
+                       "moebius_sms_per_solve": inf2["moebius_sms"], "zeta_sms": free2,
+                       "round_trip_exact": ok2,
+                       "note": "two batches' RINGCL solves side by side (one helper SM per column); "
+                               "per-batch latency is higher than the headline's"}
+                del pipe2
+        finally:
+            P.set_option("ringcl_helpers", args.ringcl_helpers)
+            P.set_option("solves_inflight", 1)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.chain import threads
@@ -656,6 +701,7 @@ def main():
             # n·k·B above counts the dense table's entries, ∞ included
             "value_nnz": 2 * info["nnz"] * GB * args.steps / (ms_max / 1e3),
             "roofline": roof, "zeta_roofline": zroof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "throughput_two_solves_inflight": two,
             "gpu_launches": launches, "clocks": clk, "round_trip_exact": ok,
             "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
                       "match": info["t_match"], "chains": info["t_chains"],

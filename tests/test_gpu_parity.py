@@ -686,6 +686,62 @@ def test_pipelined_zeta_and_moebius_on_two_streams():
         P.set_option("zeta_sms", 0)
 
 
+def test_two_solves_in_flight_vs_O2():
+    """Option solves_inflight = 2 (bench --inflight 2): two
+    batches' RINGCL solves (one helper SM per column) run side by side on two
+    streams, each with its own rank-major input lane, while the next zetas run
+    on the remaining SMs.  Möbius of arbitrary (wrapping) int64 g vs O2
+    bit-exact for every batch, and the zeta -> Möbius round trip exact."""
+    n = 120_000
+    src, dst = W.window_dag(n, 2, 64, 3, forced=True)
+    P, O = pz.Poset(n, src, dst), ChainOracle(n, src, dst)
+    B = 32
+    gs_h = [W.int_values(n, B, -2**62, 2**62, seed=70 + i) for i in range(6)]
+    fs = [W.int_values(n, B, -10**15, 10**15, seed=80 + i) for i in range(4)]
+    P.set_option("ringcl_helpers", 1)
+    P.set_option("solves_inflight", 2)
+    try:
+        P.moebius(P.zeta(dev(fs[0])))
+        torch.cuda.synchronize()
+        info = P.info()
+        assert info["moebius_kernel"] == pz.MOEB_RINGCL
+        assert 2 * info["moebius_sms"] < info["num_sms"]
+        cur = torch.cuda.current_stream()
+        s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
+        s_z = torch.cuda.Stream(priority=0)
+        for st in (s_z, *s_m):
+            st.wait_stream(cur)
+        # (a) arbitrary g, alternating streams: solves i and i+1 overlap
+        gd = [dev(g) for g in gs_h]
+        out = [torch.empty_like(g) for g in gd]
+        for st in s_m:
+            st.wait_stream(cur)
+        for i, g in enumerate(gd):
+            P.moebius(g, out=out[i], stream=s_m[i % 2])
+        torch.cuda.synchronize()
+        for i, g in enumerate(gs_h):
+            assert (host(out[i]) == O.moebius(g)).all(), i
+        # (b) the pipeline: zetas on the free SMs beside two solves
+        P.set_option("zeta_sms", info["num_sms"] - 2 * info["moebius_sms"])
+        xs = [dev(f) for f in fs]
+        zs = [torch.empty_like(x) for x in xs]
+        ys = [torch.empty_like(x) for x in xs]
+        ev = [torch.cuda.Event() for _ in xs]
+        for i, x in enumerate(xs):
+            P.zeta(x, out=zs[i], stream=s_z)
+            ev[i].record(s_z)
+            s_m[i % 2].wait_event(ev[i])
+            P.moebius(zs[i], out=ys[i], stream=s_m[i % 2])
+        torch.cuda.synchronize()
+        for i, f in enumerate(fs):
+            assert (host(zs[i]) == O.zeta(f)).all(), i
+            assert (host(ys[i]) == f).all(), i
+    finally:
+        P.set_option("zeta_sms", 0)
+        P.set_option("ringcl_helpers", 0)
+        P.set_option("solves_inflight", 1)
+
+
 @pytest.mark.parametrize("G", [1, 3])
 def test_nvls_fused_scan_row_sharded_zeta(G):
     """the row-sharded zeta with the F all-gather fused into
