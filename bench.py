@@ -62,9 +62,10 @@ def parse():
     ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
                     help="batched pipeline: batch i+1's zeta on the SMs batch i's ring-family Möbius "
                          "leaves free (two streams; auto = when the Möbius leaves SMs free)")
-    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
-                    help="Möbius solves in flight in the pipeline (2: one helper SM per column, two "
-                         "batches' solves overlap; a throughput option, not the default)")
+    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2, 3, 4],
+                    help="Möbius solves in flight in the pipeline (2: RINGCL with one helper SM per column, "
+                         "two batches' solves overlap; 3 / 4: RINGDF, one SM per column; a throughput "
+                         "option, not the default)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's global batch split over ranks (default); weak: per-rank batch")
@@ -337,9 +338,16 @@ def main():
     # Möbius use disjoint lanes, include/poset.h).  The Möbius stream has the
     # higher priority so its clusters are placed before the zeta's CTAs; the
     # zeta's persistent gather grid is sized to the free SMs (option zeta_sms).
-    if args.inflight == 2:
-        P.set_option("ringcl_helpers", 1)
-        P.set_option("solves_inflight", 2)
+    def set_inflight(nfl):
+        """Schedule for nfl solves side by side: 2 = RINGCL with one helper SM
+        per column (64 SMs per solve at B = 32), 3 / 4 = RINGDF (one SM per
+        column); 1 restores the command line's choice."""
+        P.set_option("moebius_kernel", MOEB_NAMES.index("ringdf") if nfl >= 3 else kern)
+        P.set_option("ringcl_helpers", 1 if nfl == 2 else args.ringcl_helpers)
+        P.set_option("solves_inflight", nfl)
+
+    if args.inflight >= 2:
+        set_inflight(args.inflight)
     step()   # first call: builds the lazy tables and resolves the Möbius footprint
     torch.cuda.synchronize()
     inf0 = P.info()
@@ -353,13 +361,14 @@ def main():
         # two Möbius streams, alternating: batch i+1's permutation kernel
         # (its own rank-major buffer) runs while batch i's solve is still on
         # the SMs; the library keeps the solves themselves one at a time
-        s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
+        s_m = [torch.cuda.Stream(priority=-1) for _ in range(4)]
 
     def make_pipe(inflight, budget):
         NB = 2 + (inflight - 1)                # g buffers: one per batch between zeta and Möbius
-        return {"NB": NB, "budget": budget,
+        NS = max(2, inflight)                  # Möbius streams (round-robin), one output each
+        return {"NB": NB, "NS": NS, "budget": budget,
                 "gb": [g] + [torch.empty_like(x) for _ in range(NB - 1)],
-                "ys": [y, torch.empty_like(x)] if inflight == 2 else [y, y],
+                "ys": [y] + [torch.empty_like(x) for _ in range(NS - 1)] if inflight >= 2 else [y, y],
                 "ev_z": [torch.cuda.Event() for _ in range(NB)],
                 "ev_m": [torch.cuda.Event() for _ in range(NB)]}
 
@@ -376,14 +385,15 @@ def main():
         for sm in s_m:
             sm.wait_stream(cur)
         NB, gb, ys, ev_z, ev_m = pipe["NB"], pipe["gb"], pipe["ys"], pipe["ev_z"], pipe["ev_m"]
+        NS = pipe["NS"]
         P.set_option("zeta_sms", 0)            # the prologue zeta has the whole GPU
         P.zeta(x, out=gb[0], stream=s_z)
         ev_z[0].record(s_z)
         P.set_option("zeta_sms", pipe["budget"])
         for i in range(nsteps):
-            b, sm = i % NB, s_m[i % 2]
+            b, sm = i % NB, s_m[i % NS]
             sm.wait_event(ev_z[b])
-            P.moebius(gb[b], out=ys[i % 2], stream=sm)
+            P.moebius(gb[b], out=ys[i % NS], stream=sm)
             ev_m[b].record(sm)
             if i + 1 < nsteps:
                 nb = (i + 1) % NB
@@ -400,7 +410,7 @@ def main():
     torch.cuda.synchronize()
     # correctness spot check of the timed computation (round trip)
     if wl.dtype == "i64":
-        y_last = pipe0["ys"][(args.warmup - 1) % 2] if use_pipe and args.warmup > 0 else y
+        y_last = pipe0["ys"][(args.warmup - 1) % pipe0["NS"]] if use_pipe and args.warmup > 0 else y
         ok = bool(torch.equal(y_last, x)) if (rank == 0 or not row_mode) else None
     else:
         ok = None   # fp64 Möbius on deep posets is ill-conditioned (reading G8)
@@ -625,16 +635,18 @@ def main():
     two = None
     if use_pipe and args.inflight == 1 and world == 1 and not args.no_inflight2 and \
             MOEB_NAMES[inf0["moebius_kernel"]] == "ringcl":
+        two = {}
         try:
-            P.set_option("ringcl_helpers", 1)
-            P.set_option("solves_inflight", 2)
-            step()
-            torch.cuda.synchronize()
-            inf2 = P.info()
-            free2 = inf2["num_sms"] - 2 * inf2["moebius_sms"]
-            if free2 >= 8:
-                pipe2 = make_pipe(2, free2)
-                run_steps(3, pipe2)
+            for nfl in (2, 3):
+                set_inflight(nfl)
+                step()
+                torch.cuda.synchronize()
+                inf2 = P.info()
+                free2 = inf2["num_sms"] - nfl * inf2["moebius_sms"]
+                if free2 < 8:
+                    continue
+                pipe2 = make_pipe(nfl, free2)
+                run_steps(nfl + 1, pipe2)
                 torch.cuda.synchronize()
                 ok2 = bool(torch.equal(pipe2["ys"][0], x)) if wl.dtype == "i64" else None
                 b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -643,16 +655,17 @@ def main():
                 b1.record()
                 torch.cuda.synchronize()
                 ms2 = b0.elapsed_time(b1)
-                two = {"ms_per_step": ms2 / args.steps, "value": units_step * args.steps / (ms2 / 1e3),
-                       "unit": "n·k·B gathers/s", "steps": args.steps, "solves_inflight": 2,
-                       "moebius_sms_per_solve": inf2["moebius_sms"], "zeta_sms": free2,
-                       "round_trip_exact": ok2,
-                       "note": "two batches' RINGCL solves side by side (one helper SM per column); "
-                               "per-batch latency is higher than the headline's"}
+                two[str(nfl)] = {
+                    "ms_per_step": ms2 / args.steps, "value": units_step * args.steps / (ms2 / 1e3),
+                    "unit": "n·k·B gathers/s", "steps": args.steps, "solves_inflight": nfl,
+                    "moebius_kernel": MOEB_NAMES[inf2["moebius_kernel"]],
+                    "moebius_sms_per_solve": inf2["moebius_sms"], "zeta_sms": free2, "round_trip_exact": ok2}
                 del pipe2
+            two["note"] = ("batches' solves side by side (2: RINGCL with one helper SM per column; 3: RINGDF, "
+                           "one SM per column), the zeta on the remaining SMs; per-batch latency is higher "
+                           "than the headline's")
         finally:
-            P.set_option("ringcl_helpers", args.ringcl_helpers)
-            P.set_option("solves_inflight", 1)
+            set_inflight(1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -701,7 +714,7 @@ def main():
             # n·k·B above counts the dense table's entries, ∞ included
             "value_nnz": 2 * info["nnz"] * GB * args.steps / (ms_max / 1e3),
             "roofline": roof, "zeta_roofline": zroof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "throughput_two_solves_inflight": two,
+            "throughput_solves_inflight": two,
             "gpu_launches": launches, "clocks": clk, "round_trip_exact": ok,
             "setup": {"seconds": setup_s, "ingest": info["t_ingest"], "levels": info["t_levels"],
                       "match": info["t_match"], "chains": info["t_chains"],

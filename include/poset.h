@@ -296,9 +296,12 @@ poset_status poset_query(poset_t h, poset_info *out);
  * stream leaves free (num_sms - poset_info.moebius_sms), so the gather does
  * not queue CTAs behind the Möbius (the batched pipeline);
  * "solves_inflight" (1 = default: the ring-family solve kernels of a handle
- * run one at a time; 2: calls on two streams overlap their solves -- a
- * throughput option for a stream of batches, each solve then holds its own
- * clusters of SMs);
+ * run one at a time; 2..4: calls on that many streams overlap their solves
+ * -- a throughput option for a stream of batches: each solve holds its own
+ * CTAs / clusters of SMs and its own rank-major input buffer (the buffers
+ * rotate over max(2, solves_inflight) lanes on every stream change), so the
+ * caller keeps at most that many streams' Möbius calls in flight and sizes
+ * the schedule so they fit side by side);
  * "ringcl_helpers" (RINGCL / RINGCW helper CTAs per column 1..3, 0 = auto);
  * "ringcl_chunk" (RINGCL owner stage chunk 32..256 ranks, 0 = the plan's; tuning);
  * "ringcw_sleep" (RINGCW level warps: ns between level polls, 0 = try_wait; tuning);

@@ -42,15 +42,18 @@ struct poset_s {
     //   double-buffered: a ring-family call on another stream than the
     //   previous one takes the other buffer, so its permutation kernel runs
     //   while the previous solve still reads the first);  lane S: d_stage
-    cudaEvent_t lane_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaStream_t lane_s[4] = {nullptr, nullptr, nullptr, nullptr};
-    bool lane_used[4] = {false, false, false, false};
+    //   lanes R2 / R3: d_gPx[2] / [3], used only with option solves_inflight
+    //   3 / 4 (the buffers rotate over max(2, solves_inflight) lanes)
+    static constexpr int NLANES = 6;
+    cudaEvent_t lane_ev[NLANES] = {};
+    cudaStream_t lane_s[NLANES] = {};
+    bool lane_used[NLANES] = {};
     // the ring-family solve kernels of a handle run one at a time (each
     // holds one cluster of SMs per column for the whole solve)
     cudaEvent_t solve_ev = nullptr;
     cudaStream_t solve_s = nullptr;
     bool solve_used = false;
-    int solves_inflight = 1;          // option solves_inflight (1: one solve at a time; 2: no ordering)
+    int solves_inflight = 1;          // option solves_inflight (1: one solve at a time; 2-4: no ordering)
     int gp_cur = 0;                   // d_gPx buffer of the current ring-family call
     cudaStream_t gp_last_s = nullptr;
     bool gp_any = false;
@@ -74,8 +77,8 @@ struct poset_s {
     bool sharded = false;
     int64_t m_lo = 0, m_hi = 0;
     bool gpi_delta_failed = false;
-    void *d_gPx[2] = {nullptr, nullptr};   // [B][npad] g in rank order (ring-family input)
-    size_t gPx_bytes[2] = {0, 0};
+    void *d_gPx[4] = {};   // [B][npad] g in rank order (ring-family input)
+    size_t gPx_bytes[4] = {};
     // scratch, grown on demand
     void *d_F = nullptr;
     size_t F_bytes = 0;
@@ -152,7 +155,7 @@ static void free_all(poset_s *h) {
     free_gather_pi(h->gpi);
     void *ptrs[] = {h->d_rank_user, h->d_slot, h->d_chain, h->d_lvl, h->d_child, h->d_slot_user,
                     h->d_M, h->d_child_ptr, h->d_bar, h->d_count, h->d_F, h->d_scan, h->d_part,
-                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gPx[0], h->d_gPx[1], h->ring.dbg, h->csr.ptr, h->csr.idx};
+                    h->d_stage[0], h->d_stage[1], h->ring.D, h->ring.Pn, h->ring.ru_pad, h->rws.D, h->rdf.D, h->d_gPx[0], h->d_gPx[1], h->d_gPx[2], h->d_gPx[3], h->ring.dbg, h->csr.ptr, h->csr.idx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(prev);
@@ -485,10 +488,11 @@ static bool is_device_ptr(const void *p) {
 // vector loads and stores need (the transforms stage anything else).
 static bool dev_aligned(const void *p) { return is_device_ptr(p) && ((uintptr_t)p % 32) == 0; }
 
-enum : unsigned { LANE_Z = 1, LANE_R = 2, LANE_S = 4, LANE_R1 = 8, LANE_ALL = 15 };
+enum : unsigned { LANE_Z = 1, LANE_R = 2, LANE_S = 4, LANE_R1 = 8, LANE_R2 = 16, LANE_R3 = 32, LANE_ALL = 63 };
+static const unsigned LANE_OF_GP[4] = {LANE_R, LANE_R1, LANE_R2, LANE_R3};
 
 static poset_status begin_call(poset_s *h, cudaStream_t s, unsigned lanes = LANE_ALL) {
-    for (int l = 0; l < 4; l++)
+    for (int l = 0; l < poset_s::NLANES; l++)
         if ((lanes >> l & 1) && h->lane_used[l] && s != h->lane_s[l])
             CK(cudaStreamWaitEvent(s, h->lane_ev[l], 0));
     return POSET_OK;
@@ -496,7 +500,7 @@ static poset_status begin_call(poset_s *h, cudaStream_t s, unsigned lanes = LANE
 
 static poset_status end_call(poset_s *h, cudaStream_t s, poset_status st, unsigned lanes = LANE_ALL) {
     if (st != POSET_OK) return st;
-    for (int l = 0; l < 4; l++)
+    for (int l = 0; l < poset_s::NLANES; l++)
         if (lanes >> l & 1) {
             CK(cudaEventRecord(h->lane_ev[l], s));
             h->lane_s[l] = s;
@@ -801,11 +805,11 @@ poset_status poset_moebius(poset_t h, const void *g, void *f, int64_t batch, pos
     cudaStream_t s = (cudaStream_t)stream;
     const bool ringf = ring_family(moebius_which(h, batch));
     if (ringf) {   // the other rank-major buffer when the stream changes (see poset_s::d_gPx)
-        if (h->gp_any && s != h->gp_last_s) h->gp_cur ^= 1;
+        if (h->gp_any && s != h->gp_last_s) h->gp_cur = (h->gp_cur + 1) % std::max(2, h->solves_inflight);
         h->gp_last_s = s;
         h->gp_any = true;
     }
-    const unsigned lanes = (ringf ? (h->gp_cur ? LANE_R1 : LANE_R) : LANE_Z) | (needs_staging(g, f) ? LANE_S : 0);
+    const unsigned lanes = (ringf ? LANE_OF_GP[h->gp_cur] : LANE_Z) | (needs_staging(g, f) ? LANE_S : 0);
     if ((st = begin_call(h, s, lanes))) return st;
     return end_call(h, s, run_staged(h, moebius_dev, g, f, batch, dt, s), lanes);
 }
@@ -1041,8 +1045,9 @@ poset_status poset_set_option(poset_t h, const char *key, int64_t value) {
         return POSET_OK;
     }
     if (!strcmp(key, "solves_inflight")) {   // 2: ring-family solves on two streams may overlap
-        if (value < 1 || value > 2) return fail(POSET_EINVAL, "poset_set_option: solves_inflight is 1 or 2");
+        if (value < 1 || value > 4) return fail(POSET_EINVAL, "poset_set_option: solves_inflight is 1..4");
         h->solves_inflight = (int)value;
+        h->gp_cur %= std::max(2, h->solves_inflight);
         return POSET_OK;
     }
     if (!strcmp(key, "zeta_sms")) {   // SMs the zeta's persistent grids size for (0 = all)

@@ -686,11 +686,13 @@ def test_pipelined_zeta_and_moebius_on_two_streams():
         P.set_option("zeta_sms", 0)
 
 
-def test_two_solves_in_flight_vs_O2():
-    """Option solves_inflight = 2 (bench --inflight 2): two
-    batches' RINGCL solves (one helper SM per column) run side by side on two
-    streams, each with its own rank-major input lane, while the next zetas run
-    on the remaining SMs.  Möbius of arbitrary (wrapping) int64 g vs O2
+@pytest.mark.parametrize("nfl", [2, 3, 4])
+def test_solves_in_flight_vs_O2(nfl):
+    """Option solves_inflight = 2..4 (bench --inflight): that
+    many batches' solves (2: RINGCL with one helper SM per column; 3 / 4:
+    RINGDF, one SM per column) run side by side on as many streams, each with
+    its own rank-major input lane, while the next zetas run on the remaining
+    SMs.  Möbius of arbitrary (wrapping) int64 g vs O2
     bit-exact for every batch, and the zeta -> Möbius round trip exact."""
     n = 120_000
     src, dst = W.window_dag(n, 2, 64, 3, forced=True)
@@ -698,16 +700,19 @@ def test_two_solves_in_flight_vs_O2():
     B = 32
     gs_h = [W.int_values(n, B, -2**62, 2**62, seed=70 + i) for i in range(6)]
     fs = [W.int_values(n, B, -10**15, 10**15, seed=80 + i) for i in range(4)]
-    P.set_option("ringcl_helpers", 1)
-    P.set_option("solves_inflight", 2)
+    if nfl == 2:
+        P.set_option("ringcl_helpers", 1)
+    else:
+        P.set_option("moebius_kernel", pz.MOEB_RINGDF)
+    P.set_option("solves_inflight", nfl)
     try:
         P.moebius(P.zeta(dev(fs[0])))
         torch.cuda.synchronize()
         info = P.info()
-        assert info["moebius_kernel"] == pz.MOEB_RINGCL
-        assert 2 * info["moebius_sms"] < info["num_sms"]
+        assert info["moebius_kernel"] == (pz.MOEB_RINGCL if nfl == 2 else pz.MOEB_RINGDF)
+        assert nfl * info["moebius_sms"] < info["num_sms"]
         cur = torch.cuda.current_stream()
-        s_m = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
+        s_m = [torch.cuda.Stream(priority=-1) for _ in range(nfl)]
         s_z = torch.cuda.Stream(priority=0)
         for st in (s_z, *s_m):
             st.wait_stream(cur)
@@ -717,12 +722,12 @@ def test_two_solves_in_flight_vs_O2():
         for st in s_m:
             st.wait_stream(cur)
         for i, g in enumerate(gd):
-            P.moebius(g, out=out[i], stream=s_m[i % 2])
+            P.moebius(g, out=out[i], stream=s_m[i % nfl])
         torch.cuda.synchronize()
         for i, g in enumerate(gs_h):
             assert (host(out[i]) == O.moebius(g)).all(), i
         # (b) the pipeline: zetas on the free SMs beside two solves
-        P.set_option("zeta_sms", info["num_sms"] - 2 * info["moebius_sms"])
+        P.set_option("zeta_sms", info["num_sms"] - nfl * info["moebius_sms"])
         xs = [dev(f) for f in fs]
         zs = [torch.empty_like(x) for x in xs]
         ys = [torch.empty_like(x) for x in xs]
@@ -730,8 +735,8 @@ def test_two_solves_in_flight_vs_O2():
         for i, x in enumerate(xs):
             P.zeta(x, out=zs[i], stream=s_z)
             ev[i].record(s_z)
-            s_m[i % 2].wait_event(ev[i])
-            P.moebius(zs[i], out=ys[i], stream=s_m[i % 2])
+            s_m[i % nfl].wait_event(ev[i])
+            P.moebius(zs[i], out=ys[i], stream=s_m[i % nfl])
         torch.cuda.synchronize()
         for i, f in enumerate(fs):
             assert (host(zs[i]) == O.zeta(f)).all(), i
@@ -739,6 +744,7 @@ def test_two_solves_in_flight_vs_O2():
     finally:
         P.set_option("zeta_sms", 0)
         P.set_option("ringcl_helpers", 0)
+        P.set_option("moebius_kernel", pz.MOEB_AUTO)
         P.set_option("solves_inflight", 1)
 
 
