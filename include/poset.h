@@ -41,9 +41,11 @@
  *             RINGCW) on another, both on device buffers, run concurrently,
  *             and two ring-family Möbius calls on two streams overlap the
  *             second one's permutation kernel with the first one's solve;
- *             the solve kernels of one handle always run one at a time (the
- *             library orders them by an event); everything else is
- *             serialised.  Data
+ *             the solve kernels of one handle run one at a time (the
+ *             library orders them by an event) unless option
+ *             "solves_inflight" is 2..4 (up to that many streams' solves
+ *             then overlap, each with its own rank-major lane R0..R3);
+ *             everything else is serialised.  Data
  *             dependencies between the caller's own buffers are the caller's
  *             to order (events).  A host result is valid once `stream` has
  *             synchronised (poset_sync).
