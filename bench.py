@@ -539,65 +539,70 @@ def main():
         # (copy streams + events, two buffer slots; the transforms are the
         # library's public calls on one compute stream, the intermediate g
         # stays on the device)
+        def e2e_run(NSL, budget, K):
+            """K e2e steps over NSL buffer slots (one Möbius stream per slot)."""
+            rt_ok = None
+            s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+            # pipelined: the Möbius on its own high-priority stream (see run_steps)
+            s_mb = [torch.cuda.Stream(priority=-1) for _ in range(NSL)] if use_pipe else [s_cmp] * NSL
+            xin = [torch.empty_like(x) for _ in range(NSL)]
+            yout = [torch.empty_like(x) for _ in range(NSL)]
+            gd2 = [torch.empty_like(x) for _ in range(NSL)] if use_pipe else [torch.empty_like(x)] * NSL
+            res = [torch.empty_like(fp).pin_memory() for _ in range(NSL)]
+            ev = lambda: torch.cuda.Event()
+            in_done, in_free, out_done, out_free = [ev() for _ in range(NSL)], [ev() for _ in range(NSL)], \
+                [ev() for _ in range(NSL)], [ev() for _ in range(NSL)]
+            z_done, g_free = [ev() for _ in range(NSL)], [ev() for _ in range(NSL)]
+
+            def pipelined(steps):
+                P.set_option("zeta_sms", budget)
+                for i in range(steps):
+                    sl = i % NSL
+                    with torch.cuda.stream(s_in):
+                        if i >= NSL:
+                            s_in.wait_event(in_free[sl])
+                        xin[sl].copy_(fp, non_blocking=True)
+                        in_done[sl].record(s_in)
+                    s_cmp.wait_event(in_done[sl])
+                    if i >= NSL and use_pipe:
+                        s_cmp.wait_event(g_free[sl])
+                    P.zeta(xin[sl], out=gd2[sl], stream=s_cmp)
+                    in_free[sl].record(s_cmp)
+                    z_done[sl].record(s_cmp)
+                    s_mb[sl].wait_event(z_done[sl])
+                    if i >= NSL:
+                        s_mb[sl].wait_event(out_free[sl])
+                    P.moebius(gd2[sl], out=yout[sl], stream=s_mb[sl])
+                    g_free[sl].record(s_mb[sl])
+                    out_done[sl].record(s_mb[sl])
+                    with torch.cuda.stream(s_out):
+                        s_out.wait_event(out_done[sl])
+                        res[sl].copy_(yout[sl], non_blocking=True)
+                        out_free[sl].record(s_out)
+                P.set_option("zeta_sms", 0)
+
+            pipelined(NSL)
+            torch.cuda.synchronize()
+            if wl.dtype == "i64":
+                rt_ok = bool((res[NSL - 1].numpy() == f_host).all())
+            if world > 1:
+                torch.distributed.barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_in.wait_stream(torch.cuda.current_stream())
+            a0.record(s_in)
+            pipelined(K)
+            s_in.wait_stream(s_out)
+            for sm in s_mb:
+                s_in.wait_stream(sm)
+            a1.record(s_in)
+            torch.cuda.synchronize()
+            ems = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
+            return float(ems.item()), rt_ok
+
         K = args.e2e_steps
-        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        # pipelined: the Möbius on its own high-priority stream (see run_steps)
-        s_mb = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)] if use_pipe else [s_cmp] * 2
-        xin = [torch.empty_like(x) for _ in range(2)]
-        yout = [torch.empty_like(x) for _ in range(2)]
-        gd2 = [torch.empty_like(x) for _ in range(2)] if use_pipe else [torch.empty_like(x)] * 2
-        res = [torch.empty_like(fp).pin_memory() for _ in range(2)]
-        ev = lambda: torch.cuda.Event()
-        in_done, in_free, out_done, out_free = [ev() for _ in range(2)], [ev() for _ in range(2)], \
-            [ev() for _ in range(2)], [ev() for _ in range(2)]
-        z_done, g_free = [ev() for _ in range(2)], [ev() for _ in range(2)]
-
-        def pipelined(steps):
-            P.set_option("zeta_sms", zeta_budget)
-            for i in range(steps):
-                sl = i % 2
-                with torch.cuda.stream(s_in):
-                    if i >= 2:
-                        s_in.wait_event(in_free[sl])
-                    xin[sl].copy_(fp, non_blocking=True)
-                    in_done[sl].record(s_in)
-                s_cmp.wait_event(in_done[sl])
-                if i >= 2 and use_pipe:
-                    s_cmp.wait_event(g_free[sl])
-                P.zeta(xin[sl], out=gd2[sl], stream=s_cmp)
-                in_free[sl].record(s_cmp)
-                z_done[sl].record(s_cmp)
-                s_mb[sl].wait_event(z_done[sl])
-                if i >= 2:
-                    s_mb[sl].wait_event(out_free[sl])
-                P.moebius(gd2[sl], out=yout[sl], stream=s_mb[sl])
-                g_free[sl].record(s_mb[sl])
-                out_done[sl].record(s_mb[sl])
-                with torch.cuda.stream(s_out):
-                    s_out.wait_event(out_done[sl])
-                    res[sl].copy_(yout[sl], non_blocking=True)
-                    out_free[sl].record(s_out)
-            P.set_option("zeta_sms", 0)
-
-        pipelined(2)
-        torch.cuda.synchronize()
-        if wl.dtype == "i64":
-            rt_ok = bool((res[1].numpy() == f_host).all())
-        if world > 1:
-            torch.distributed.barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s_in.wait_stream(torch.cuda.current_stream())
-        a0.record(s_in)
-        pipelined(K)
-        s_in.wait_stream(s_out)
-        for sm in s_mb:
-            s_in.wait_stream(sm)
-        a1.record(s_in)
-        torch.cuda.synchronize()
-        ems = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
-        ems = float(ems.item())
+        ems, rt_ok = e2e_run(2, zeta_budget, K)
         e2e = {"value": units_step * K / (ems / 1e3), "unit": "n·k·B gathers/s",
                "h2d_bytes_per_step": n * GB * 8, "d2h_bytes_per_step": n * GB * 8,
                "ms_per_step": ems / K, "steps": K,
@@ -608,7 +613,24 @@ def main():
                                            ", one compute stream") +
                         "), result -> pinned host copy; copies on their own streams, overlapping the "
                         "neighbouring steps' transforms")}
-        del xin, yout, gd2, res
+        # the same with three batches' RINGDF solves in flight (three slots)
+        if use_pipe and args.inflight == 1 and world == 1 and not args.no_inflight2 and \
+                MOEB_NAMES[inf0["moebius_kernel"]] == "ringcl":
+            try:
+                set_inflight(3)
+                step()
+                torch.cuda.synchronize()
+                inf3 = P.info()
+                free3 = inf3["num_sms"] - 3 * inf3["moebius_sms"]
+                if free3 >= 8:
+                    K3 = 3 * max(K // 3, 1)
+                    ems3, ok3 = e2e_run(3, free3, K3)
+                    e2e["three_solves_inflight"] = {
+                        "value": units_step * K3 / (ems3 / 1e3), "ms_per_step": ems3 / K3, "steps": K3,
+                        "round_trip_exact": ok3, "moebius_kernel": MOEB_NAMES[inf3["moebius_kernel"]],
+                        "zeta_sms": free3}
+            finally:
+                set_inflight(1)
         # (b) context: both transforms staged through host memory by the library
         # itself (zeta host -> host, Möbius host -> host, serial)
         gp = torch.empty_like(fp).pin_memory()
